@@ -1,0 +1,983 @@
+// Host side of the B200 middle-MPO engine: device-resident chains, the
+// orchestration of each chain operation as a stream-ordered sequence of
+// kernels, and the extern "C" boundary declared in include/mirrorbreak_b200.h.
+//
+// Every operation follows the reference's numerical call sequence
+// (/root/reference/pkg/src/mirrorbreak/chains.py): the same orthogonality
+// center moves, the same blob contractions, the same truncated re-splits, so
+// that every truncation decision is taken on the same operator. QR steps are
+// realized as untruncated SVD-based isometric splits (same shapes as the
+// reference's reduced QR; only the gauge differs, and all decisions are
+// gauge-invariant).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mb_kernels.cuh"
+#include "mirrorbreak_b200.h"
+
+namespace mb {
+
+struct MbError : std::runtime_error {
+  int code;
+  MbError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+static thread_local std::string g_err;
+
+static void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw MbError(MB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  ~DevBuf();
+};
+using Buf = std::shared_ptr<DevBuf>;
+
+enum ProfClass { P_GEMM = 0, P_GATE = 1, P_SVD_SMALL = 2, P_SVD_LARGE = 3, P_EMIT = 4, P_OTHER = 5 };
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double flops;
+};
+
+struct Engine {
+  bool ready = false;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  // pinned host scratch for readbacks
+  int64_t* h_info = nullptr;  // 3 * kSlots
+  double* h_disc = nullptr;   // kSlots
+  double* h_scalar = nullptr; // 4
+  int* h_flag = nullptr;
+  // device scalars
+  Buf d_info, d_disc, d_flag, d_partial, d_scalar;
+  // grow-only scratch
+  static constexpr int kSlots = 4;
+  Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots];
+  Buf carry, env[2], amp, misc;
+  long long counters[6] = {0, 0, 0, 0, 0, 0};
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+};
+
+static Engine E;
+
+DevBuf::~DevBuf() {
+  if (p) cudaFreeAsync(p, s ? s : E.stream);
+}
+
+static Buf alloc(size_t bytes) {
+  auto b = std::make_shared<DevBuf>();
+  b->bytes = bytes;
+  b->s = E.stream;
+  if (bytes) ck(cudaMallocAsync(&b->p, bytes, E.stream), "cudaMallocAsync");
+  return b;
+}
+
+static void* grow(Buf& b, size_t bytes) {
+  if (!b || b->bytes < bytes) {
+    size_t want = bytes + bytes / 4 + 256;
+    b = alloc(want);
+  }
+  return b->p;
+}
+
+static void sync() {
+  E.counters[3]++;
+  ck(cudaStreamSynchronize(E.stream), "cudaStreamSynchronize");
+}
+
+// ---- profiling ---------------------------------------------------------
+static cudaEvent_t ev_get() {
+  if (!E.pool.empty()) {
+    cudaEvent_t e = E.pool.back();
+    E.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+struct ProfScope {
+  int cls;
+  double flops;
+  cudaEvent_t a = nullptr;
+  ProfScope(int c, double f) : cls(c), flops(f) {
+    if (E.prof) {
+      a = ev_get();
+      cudaEventRecord(a, E.stream);
+    }
+  }
+  ~ProfScope() {
+    if (E.prof) {
+      cudaEvent_t b = ev_get();
+      cudaEventRecord(b, E.stream);
+      E.recs.push_back({cls, a, b, flops});
+    }
+  }
+};
+
+}  // namespace mb
+
+struct mb_chain {
+  struct Site {
+    mb::Buf b;
+    int64_t l, r;
+  };
+  int n = 0, d = 4, dtype = MB_C128;
+  std::vector<Site> s;
+  double log_norm = 0.0;
+  int center = -1;
+};
+
+namespace mb {
+
+using Site = mb_chain::Site;
+
+template <typename R>
+static cx<R>* P(const Site& s) {
+  return reinterpret_cast<cx<R>*>(s.b->p);
+}
+
+template <typename R>
+static Site new_site(int64_t l, int d, int64_t r) {
+  return Site{alloc((size_t)(l * d * r) * sizeof(cx<R>)), l, r};
+}
+
+static void require(bool ok, const char* msg) {
+  if (!ok) throw MbError(MB_ERR_ARG, msg);
+}
+
+static double gemm_flops(int64_t M, int64_t N, int64_t K) { return 8.0 * M * N * K; }
+
+template <typename R>
+static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64_t lda,
+                 const cx<R>* B, int64_t ldb, cx<R>* C, int64_t ldc) {
+  ProfScope ps(P_GEMM, gemm_flops(M, N, K));
+  launch_gemm<R>(ct, M, N, K, A, lda, B, ldb, C, ldc, E.stream);
+}
+
+// ---- SVD orchestration ---------------------------------------------------
+
+template <typename R>
+static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double eps, int64_t chi,
+                          bool want_v) {
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  SvdJob<R> j;
+  j.A = A;
+  j.X = (cx<R>*)grow(E.X[slot], (size_t)(p * q) * sizeof(cx<R>));
+  j.V = want_v ? (cx<R>*)grow(E.V[slot], (size_t)(p * p) * sizeof(cx<R>)) : nullptr;
+  j.sig = (R*)grow(E.sig[slot], (size_t)(2 * p) * sizeof(R));
+  j.perm = (int*)grow(E.perm[slot], (size_t)p * sizeof(int));
+  j.m = m;
+  j.n = n;
+  j.eps = eps;
+  j.chi = chi;
+  j.info = reinterpret_cast<int64_t*>(E.d_info->p) + 3 * slot;
+  j.disc = reinterpret_cast<double*>(E.d_disc->p) + slot;
+  if (p > E.counters[5]) E.counters[5] = p;
+  return j;
+}
+
+template <typename R>
+static void run_jobs(SvdJob<R>* jobs, int nj) {
+  std::vector<SvdJob<R>> small;
+  int maxp = 0;
+  for (int i = 0; i < nj; ++i) {
+    int64_t p = jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n;
+    if (p <= kSmallP) {
+      small.push_back(jobs[i]);
+      if (p > maxp) maxp = (int)p;
+    }
+  }
+  if (!small.empty()) {
+    double fl = 0;
+    for (auto& j : small) {
+      double p = (double)(j.m < j.n ? j.m : j.n), q = (double)(j.m < j.n ? j.n : j.m);
+      fl += 2.0 * 8.0 * p * p * q;  // one Gram + one rotation pass (lower bound)
+    }
+    ProfScope ps(P_SVD_SMALL, fl);
+    launch_svd_small<R>(small.data(), (int)small.size(), maxp, E.stream);
+    E.counters[0] += (long long)small.size();
+  }
+  for (int i = 0; i < nj; ++i) {
+    int64_t p = jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n;
+    if (p > kSmallP) {
+      double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
+      ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * (double)p * (double)p * q);
+      svd_large<R>(jobs[i], reinterpret_cast<int*>(E.d_flag->p), E.h_flag, E.stream);
+      E.counters[1]++;
+      E.counters[3]++;
+    }
+  }
+}
+
+// Read back kept ranks (and discarded weights) of the first `ns` slots.
+static void read_info(int ns) {
+  ck(cudaMemcpyAsync(E.h_info, E.d_info->p, sizeof(int64_t) * 3 * ns, cudaMemcpyDeviceToHost,
+                     E.stream),
+     "readback info");
+  ck(cudaMemcpyAsync(E.h_disc, E.d_disc->p, sizeof(double) * ns, cudaMemcpyDeviceToHost, E.stream),
+     "readback disc");
+  sync();
+  for (int i = 0; i < ns; ++i)
+    if (E.h_info[3 * i + 1]) E.counters[4]++;
+}
+
+template <typename R>
+static void emit(const SvdJob<R>& j, int64_t k, cx<R>* U, bool su, cx<R>* V, bool sv) {
+  ProfScope ps(P_EMIT, 0.0);
+  launch_emit<R>(j, k, U, su, V, sv, E.stream);
+}
+
+template <typename R>
+static double norm_of(const cx<R>* buf, int64_t n) {
+  void* part = grow(E.d_partial, 256 * sizeof(double));
+  {
+    ProfScope ps(P_OTHER, 0.0);
+    launch_sumsq<R>(buf, n, (double*)part, (double*)E.d_scalar->p, E.stream);
+  }
+  ck(cudaMemcpyAsync(E.h_scalar, E.d_scalar->p, sizeof(double), cudaMemcpyDeviceToHost, E.stream),
+     "readback norm");
+  sync();
+  return std::sqrt(E.h_scalar[0]);
+}
+
+// ---- canonical-form plumbing (chains.py:110-145) ----------------------------
+
+// Left-orthogonalize site i, pushing the remainder into site i+1 (chains.py:110).
+template <typename R>
+static void push_right(mb_chain& c, int i) {
+  const int d = c.d;
+  Site A = c.s[i], B = c.s[i + 1];
+  const int64_t m = A.l * d, n = A.r, rn = (int64_t)d * B.r;
+  Site nA, nB;
+  if (m < n) {  // wide: Q = I_m, R = A
+    nA = new_site<R>(A.l, d, m);
+    {
+      ProfScope ps(P_OTHER, 0.0);
+      launch_identity<R>(P<R>(nA), m, E.stream);
+    }
+    nB = new_site<R>(m, d, B.r);
+    gemm<R>(false, m, rn, n, P<R>(A), n, P<R>(B), rn, P<R>(nB), rn);
+  } else {
+    SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
+    run_jobs<R>(&j, 1);
+    nA = new_site<R>(A.l, d, n);
+    cx<R>* Rm = (cx<R>*)grow(E.carry, (size_t)(n * n) * sizeof(cx<R>));
+    emit<R>(j, n, P<R>(nA), false, Rm, true);
+    nB = new_site<R>(n, d, B.r);
+    gemm<R>(false, n, rn, n, Rm, n, P<R>(B), rn, P<R>(nB), rn);
+  }
+  c.s[i] = nA;
+  c.s[i + 1] = nB;
+}
+
+// Right-orthogonalize site i, pushing the remainder into site i-1 (chains.py:119).
+template <typename R>
+static void push_left(mb_chain& c, int i) {
+  const int d = c.d;
+  Site A = c.s[i], Pv = c.s[i - 1];
+  const int64_t m = A.l, n = (int64_t)d * A.r, pm = Pv.l * d;
+  Site nA, nP;
+  if (m > n) {  // tall: Q = I_n, L = A
+    nA = new_site<R>(n, d, A.r);
+    {
+      ProfScope ps(P_OTHER, 0.0);
+      launch_identity<R>(P<R>(nA), n, E.stream);
+    }
+    nP = new_site<R>(Pv.l, d, n);
+    gemm<R>(false, pm, n, m, P<R>(Pv), m, P<R>(A), n, P<R>(nP), n);
+  } else {
+    SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
+    run_jobs<R>(&j, 1);
+    nA = new_site<R>(m, d, A.r);
+    cx<R>* L = (cx<R>*)grow(E.carry, (size_t)(m * m) * sizeof(cx<R>));
+    emit<R>(j, m, L, true, P<R>(nA), false);
+    nP = new_site<R>(Pv.l, d, m);
+    gemm<R>(false, pm, m, m, P<R>(Pv), m, L, m, P<R>(nP), m);
+  }
+  c.s[i] = nA;
+  c.s[i - 1] = nP;
+}
+
+template <typename R>
+static void move_center(mb_chain& c, int target) {
+  require(target >= 0 && target < c.n, "center target out of range");
+  if (c.center < 0) {
+    for (int i = 0; i < target; ++i) push_right<R>(c, i);
+    for (int i = c.n - 1; i > target; --i) push_left<R>(c, i);
+  } else if (c.center < target) {
+    for (int i = c.center; i < target; ++i) push_right<R>(c, i);
+  } else {
+    for (int i = c.center; i > target; --i) push_left<R>(c, i);
+  }
+  c.center = target;
+}
+
+// ---- two-site operations ------------------------------------------------------
+
+template <typename R>
+static Gate4<R> swap_gate() {
+  Gate4<R> g;
+  for (int i = 0; i < 16; ++i) g.g[i] = mk<R>(0, 0);
+  g.g[0 * 4 + 0] = g.g[1 * 4 + 2] = g.g[2 * 4 + 1] = g.g[3 * 4 + 3] = mk<R>(1, 0);
+  return g;
+}
+
+// theta (4l x 4r) = site_b (4l x chi) @ site_{b+1} (chi x 4r)   (chains.py:170)
+template <typename R>
+static cx<R>* blob(mb_chain& c, int b, int slot, int64_t& l, int64_t& r) {
+  Site A = c.s[b], B = c.s[b + 1];
+  l = A.l;
+  r = B.r;
+  const int64_t M = 4 * l, N = 4 * r, K = A.r;
+  cx<R>* th = (cx<R>*)grow(E.theta[slot], (size_t)(M * N) * sizeof(cx<R>));
+  gemm<R>(false, M, N, K, P<R>(A), K, P<R>(B), N, th, N);
+  return th;
+}
+
+// Truncated re-split of theta into sites (b, b+1), S on the right (chains.py:157-167).
+template <typename R>
+static void resplit(mb_chain& c, int b, cx<R>* th, int64_t l, int64_t r, double eps, int64_t chi) {
+  SvdJob<R> j = make_job<R>(0, th, 4 * l, 4 * r, eps, chi, true);
+  run_jobs<R>(&j, 1);
+  read_info(1);
+  const int64_t k = E.h_info[0];
+  Site nA = new_site<R>(l, 4, k), nB = new_site<R>(k, 4, r);
+  emit<R>(j, k, P<R>(nA), false, P<R>(nB), true);
+  c.s[b] = nA;
+  c.s[b + 1] = nB;
+  c.center = b + 1;
+}
+
+template <typename R>
+static void absorb_2q(mb_chain& c, int lo, const double* g4, int side, double eps, int64_t chi) {
+  require(c.d == 4, "absorb on a non-operator chain");
+  require(lo >= 0 && lo + 1 < c.n, "two-qubit gate out of range");
+  require(side == MB_SIDE_LEFT || side == MB_SIDE_RIGHT, "side must be left or right");
+  move_center<R>(c, lo);
+  int64_t l, r;
+  cx<R>* th = blob<R>(c, lo, 0, l, r);
+  Gate4<R> g;
+  for (int i = 0; i < 16; ++i) g.g[i] = mk<R>((R)g4[2 * i], (R)g4[2 * i + 1]);
+  {
+    ProfScope ps(P_GATE, 0.0);
+    launch_gate2<R>(th, g, l, r, side == MB_SIDE_LEFT, E.stream);
+  }
+  resplit<R>(c, lo, th, l, r, eps, chi);
+}
+
+template <typename R>
+static void absorb_1q(mb_chain& c, int q, const double* u2, int side) {
+  require(c.d == 4, "absorb on a non-operator chain");
+  require(q >= 0 && q < c.n, "qubit out of range");
+  require(side == MB_SIDE_LEFT || side == MB_SIDE_RIGHT, "side must be left or right");
+  Gate2<R> u;
+  for (int i = 0; i < 4; ++i) u.g[i] = mk<R>((R)u2[2 * i], (R)u2[2 * i + 1]);
+  Site A = c.s[q];
+  Site nA = new_site<R>(A.l, 4, A.r);
+  {
+    ProfScope ps(P_GATE, 0.0);
+    launch_gate1<R>(P<R>(A), P<R>(nA), u, A.l, A.r, side == MB_SIDE_LEFT, E.stream);
+  }
+  c.s[q] = nA;  // a unitary on one site keeps the canonical structure (chains.py:200)
+}
+
+template <typename R>
+static void pair_swap(mb_chain& c, int b, bool top, bool bottom, double eps, int64_t chi,
+                      bool recenter) {
+  require(c.d == 4, "swap on a non-operator chain");
+  require(b >= 0 && b + 1 < c.n, "bond out of range");
+  if (recenter) move_center<R>(c, b);
+  int64_t l, r;
+  cx<R>* th = blob<R>(c, b, 0, l, r);
+  Gate4<R> sw = swap_gate<R>();
+  if (top) {
+    ProfScope ps(P_GATE, 0.0);
+    launch_gate2<R>(th, sw, l, r, true, E.stream);
+  }
+  if (bottom) {
+    ProfScope ps(P_GATE, 0.0);
+    launch_gate2<R>(th, sw, l, r, false, E.stream);
+  }
+  resplit<R>(c, b, th, l, r, eps, chi);
+}
+
+template <typename R>
+static void swap_extents(mb_chain& c, int b, int ns, const int* sides, double eps, int64_t chi,
+                         int64_t* out) {
+  require(c.d == 4, "swap on a non-operator chain");
+  require(b >= 0 && b + 1 < c.n, "bond out of range");
+  require(ns >= 1 && ns <= 3, "1..3 sides");
+  int64_t l, r;
+  cx<R>* th0 = blob<R>(c, b, 3, l, r);
+  const int64_t M = 4 * l, N = 4 * r;
+  Gate4<R> sw = swap_gate<R>();
+  SvdJob<R> jobs[3];
+  for (int k = 0; k < ns; ++k) {
+    cx<R>* th = (cx<R>*)grow(E.theta[k], (size_t)(M * N) * sizeof(cx<R>));
+    ck(cudaMemcpyAsync(th, th0, (size_t)(M * N) * sizeof(cx<R>), cudaMemcpyDeviceToDevice,
+                       E.stream),
+       "copy blob");
+    int sd = sides[k];
+    require(sd >= 0 && sd <= 2, "bad side");
+    ProfScope ps(P_GATE, 0.0);
+    if (sd == MB_SIDE_LEFT || sd == MB_SIDE_BOTH) launch_gate2<R>(th, sw, l, r, true, E.stream);
+    if (sd == MB_SIDE_RIGHT || sd == MB_SIDE_BOTH) launch_gate2<R>(th, sw, l, r, false, E.stream);
+    jobs[k] = make_job<R>(k, th, M, N, eps, chi, false);
+  }
+  run_jobs<R>(jobs, ns);
+  read_info(ns);
+  for (int k = 0; k < ns; ++k) out[k] = E.h_info[3 * k];
+}
+
+// Right-to-left truncation step at site i (chains.py:273-280, 310-315).
+template <typename R>
+static void truncate_left(mb_chain& c, int i, double eps, int64_t chi) {
+  const int d = c.d;
+  Site A = c.s[i], Pv = c.s[i - 1];
+  const int64_t m = A.l, n = (int64_t)d * A.r;
+  SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, eps, chi, true);
+  run_jobs<R>(&j, 1);
+  read_info(1);
+  const int64_t k = E.h_info[0];
+  Site nA = new_site<R>(k, d, A.r);
+  cx<R>* carry = (cx<R>*)grow(E.carry, (size_t)(m * k) * sizeof(cx<R>));
+  emit<R>(j, k, carry, true, P<R>(nA), false);
+  Site nP = new_site<R>(Pv.l, d, k);
+  gemm<R>(false, Pv.l * d, k, m, P<R>(Pv), m, carry, k, P<R>(nP), k);
+  c.s[i] = nA;
+  c.s[i - 1] = nP;
+}
+
+// Scale site 0 by 1/f, copying first if the buffer is shared with a clone.
+template <typename R>
+static void scale_site0(mb_chain& c, double f) {
+  Site A = c.s[0];
+  int64_t ne = A.l * c.d * A.r;
+  if (A.b.use_count() > 1) {
+    Site nA = new_site<R>(A.l, c.d, A.r);
+    ck(cudaMemcpyAsync(P<R>(nA), P<R>(A), (size_t)ne * sizeof(cx<R>), cudaMemcpyDeviceToDevice,
+                       E.stream),
+       "copy site");
+    c.s[0] = nA;
+  }
+  ProfScope ps(P_OTHER, 0.0);
+  launch_scale<R>(P<R>(c.s[0]), ne, 1.0 / f, E.stream);
+}
+
+template <typename R>
+static void compress(mb_chain& c, double eps, int64_t chi) {
+  for (int i = 0; i + 1 < c.n; ++i) push_right<R>(c, i);
+  for (int i = c.n - 1; i > 0; --i) truncate_left<R>(c, i, eps, chi);
+  Site A = c.s[0];
+  double f = norm_of<R>(P<R>(A), A.l * c.d * A.r);
+  if (f == 0.0) throw MbError(MB_ERR_NUMERIC, "compress reached an all-zero chain");
+  scale_site0<R>(c, f);
+  c.log_norm += std::log(f);
+  c.center = 0;
+}
+
+template <typename R>
+static double frob(const mb_chain& c) {
+  if (c.center >= 0) {
+    Site A = c.s[c.center];
+    return norm_of<R>(P<R>(A), A.l * c.d * A.r);
+  }
+  mb_chain w = c;
+  move_center<R>(w, 0);
+  Site A = w.s[0];
+  return norm_of<R>(P<R>(A), A.l * w.d * A.r);
+}
+
+template <typename R>
+static mb_chain* apply_to_zero(const mb_chain& c, double eps, int64_t chi) {
+  require(c.d == 4, "apply_to_zero needs an operator chain");
+  const double scale = frob<R>(c);
+  auto* m = new mb_chain();
+  m->n = c.n;
+  m->d = 2;
+  m->dtype = c.dtype;
+  m->log_norm = c.log_norm;
+  m->center = -1;
+  for (int i = 0; i < c.n; ++i) {
+    Site A = c.s[i];
+    Site nA = new_site<R>(A.l, 2, A.r);
+    ProfScope ps(P_OTHER, 0.0);
+    launch_slice_b0<R>(P<R>(A), P<R>(nA), A.l, A.r, E.stream);
+    m->s.push_back(nA);
+  }
+  try {
+    for (int i = 0; i + 1 < m->n; ++i) push_right<R>(*m, i);
+    for (int i = m->n - 1; i > 0; --i) truncate_left<R>(*m, i, eps, chi);
+    Site A = m->s[0];
+    double f = norm_of<R>(P<R>(A), A.l * 2 * A.r);
+    double expected = scale / std::pow(2.0, m->n / 2.0);
+    if (f < 1e-12 * expected)
+      throw MbError(MB_ERR_NUMERIC, "all-zero column norm collapsed below 1e-12 of the expected "
+                                    "scale; upstream truncation destroyed the state");
+    scale_site0<R>(*m, f);
+    m->log_norm = c.log_norm + std::log(f);
+    m->center = 0;
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  return m;
+}
+
+// chains.py:327-344
+template <typename R>
+static double right_canonical(mb_chain& w) {
+  int start = w.center >= 0 ? w.center : w.n - 1;
+  if (w.center < 0)
+    for (int i = 0; i + 1 < w.n; ++i) push_right<R>(w, i);
+  for (int i = start; i > 0; --i) push_left<R>(w, i);
+  w.center = 0;
+  Site A = w.s[0];
+  return norm_of<R>(P<R>(A), A.l * w.d * A.r);
+}
+
+template <typename R>
+static void peak(const mb_chain& psi, uint8_t* bits, double* probs) {
+  require(psi.d == 2, "peak extraction needs a state chain");
+  mb_chain w = psi;
+  double nrm = right_canonical<R>(w);
+  if (std::fabs(nrm - 1.0) > 1e-6) throw MbError(MB_ERR_NUMERIC, "state is not normalized");
+  const int n = w.n;
+  std::vector<const cx<R>*> ptrs(n);
+  std::vector<int64_t> dims(3 * n + 1);
+  int64_t maxb = 1;
+  for (int i = 0; i < n; ++i) {
+    ptrs[i] = P<R>(w.s[i]);
+    dims[3 * i] = w.s[i].l;
+    dims[3 * i + 1] = 2;
+    dims[3 * i + 2] = w.s[i].r;
+    maxb = std::max(maxb, std::max(w.s[i].l, w.s[i].r));
+  }
+  dims[3 * n] = maxb;
+  Buf dp = alloc(n * sizeof(void*)), dd = alloc(dims.size() * sizeof(int64_t));
+  Buf db = alloc(n), dpr = alloc(n * sizeof(double));
+  Buf scr = alloc((size_t)(3 * maxb) * sizeof(cx<R>));
+  ck(cudaMemcpyAsync(dp->p, ptrs.data(), n * sizeof(void*), cudaMemcpyHostToDevice, E.stream), "h2d");
+  ck(cudaMemcpyAsync(dd->p, dims.data(), dims.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                     E.stream),
+     "h2d");
+  {
+    ProfScope ps(P_OTHER, 0.0);
+    launch_peak<R>((const cx<R>* const*)dp->p, (const int64_t*)dd->p, n, maxb, (uint8_t*)db->p,
+                   (double*)dpr->p, (cx<R>*)scr->p, E.stream);
+  }
+  ck(cudaMemcpyAsync(bits, db->p, n, cudaMemcpyDeviceToHost, E.stream), "d2h");
+  ck(cudaMemcpyAsync(probs, dpr->p, n * sizeof(double), cudaMemcpyDeviceToHost, E.stream), "d2h");
+  sync();
+}
+
+template <typename R>
+static void sample(const mb_chain& psi, int64_t shots, const double* uni, uint8_t* bits) {
+  require(psi.d == 2, "sampling needs a state chain");
+  require(shots >= 1, "shots must be positive");
+  mb_chain w = psi;
+  double nrm = right_canonical<R>(w);
+  if (std::fabs(nrm - 1.0) > 1e-6) throw MbError(MB_ERR_NUMERIC, "state is not normalized");
+  const int n = w.n;
+  int64_t maxb = 1;
+  for (int i = 0; i < n; ++i) maxb = std::max(maxb, w.s[i].r);
+  Buf du = alloc((size_t)(n * shots) * sizeof(double));
+  Buf db = alloc((size_t)(n * shots));
+  ck(cudaMemcpyAsync(du->p, uni, (size_t)(n * shots) * sizeof(double), cudaMemcpyHostToDevice,
+                     E.stream),
+     "h2d");
+  cx<R>* envA = (cx<R>*)grow(E.env[0], (size_t)(shots * maxb) * sizeof(cx<R>));
+  cx<R>* envB = (cx<R>*)grow(E.env[1], (size_t)(shots * maxb) * sizeof(cx<R>));
+  cx<R>* amp = (cx<R>*)grow(E.amp, (size_t)(shots * 2 * maxb) * sizeof(cx<R>));
+  std::vector<cx<R>> ones(shots, mk<R>(1, 0));
+  ck(cudaMemcpyAsync(envA, ones.data(), shots * sizeof(cx<R>), cudaMemcpyHostToDevice, E.stream),
+     "h2d");
+  for (int i = 0; i < n; ++i) {
+    Site S = w.s[i];
+    gemm<R>(false, shots, 2 * S.r, S.l, envA, S.l, P<R>(S), 2 * S.r, amp, 2 * S.r);
+    {
+      ProfScope ps(P_OTHER, 0.0);
+      launch_sample_pick<R>(amp, shots, S.r, (const double*)du->p + (size_t)i * shots,
+                            (uint8_t*)db->p + i, n, envB, E.stream);
+    }
+    std::swap(envA, envB);
+  }
+  ck(cudaMemcpyAsync(bits, db->p, (size_t)(n * shots), cudaMemcpyDeviceToHost, E.stream), "d2h");
+  sync();
+}
+
+// ---- host <-> device ---------------------------------------------------------
+
+template <typename R>
+static void upload(const double* host, cx<R>* dst, int64_t ne) {
+  if (ne == 0) return;
+  if (sizeof(R) == sizeof(double)) {
+    ck(cudaMemcpyAsync(dst, host, (size_t)ne * 16, cudaMemcpyHostToDevice, E.stream), "h2d");
+  } else {
+    void* tmp = grow(E.misc, (size_t)ne * 16);
+    ck(cudaMemcpyAsync(tmp, host, (size_t)ne * 16, cudaMemcpyHostToDevice, E.stream), "h2d");
+    launch_convert<R>(tmp, true, dst, ne, E.stream);
+  }
+}
+
+template <typename R>
+static void download(const cx<R>* src, double* host, int64_t ne) {
+  if (ne == 0) return;
+  if (sizeof(R) == sizeof(double)) {
+    ck(cudaMemcpyAsync(host, src, (size_t)ne * 16, cudaMemcpyDeviceToHost, E.stream), "d2h");
+  } else {
+    cx<double>* tmp = (cx<double>*)grow(E.misc, (size_t)ne * 16);
+    launch_convert<double>(src, false, tmp, ne, E.stream);
+    ck(cudaMemcpyAsync(host, tmp, (size_t)ne * 16, cudaMemcpyDeviceToHost, E.stream), "d2h");
+  }
+}
+
+template <typename R>
+static mb_chain* from_host(int n, int d, int dtype, const int64_t* bonds, const double* data,
+                           double log_norm, int center) {
+  auto* c = new mb_chain();
+  c->n = n;
+  c->d = d;
+  c->dtype = dtype;
+  c->log_norm = log_norm;
+  c->center = center;
+  int64_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    Site s = new_site<R>(bonds[i], d, bonds[i + 1]);
+    int64_t ne = bonds[i] * d * bonds[i + 1];
+    upload<R>(data + 2 * off, P<R>(s), ne);
+    off += ne;
+    c->s.push_back(s);
+  }
+  sync();
+  return c;
+}
+
+template <typename R>
+static void to_host(const mb_chain& c, double* data) {
+  int64_t off = 0;
+  for (int i = 0; i < c.n; ++i) {
+    int64_t ne = c.s[i].l * c.d * c.s[i].r;
+    download<R>(P<R>(c.s[i]), data + 2 * off, ne);
+    sync();  // the conversion scratch is reused per site
+    off += ne;
+  }
+}
+
+template <typename R>
+static void svd_host(const double* a, int64_t m, int64_t n, double eps, int64_t chi, double* u,
+                     double* s, double* v, int64_t* rank, double* disc) {
+  Buf dA = alloc((size_t)(m * n) * sizeof(cx<R>));
+  upload<R>(a, (cx<R>*)dA->p, m * n);
+  SvdJob<R> j = make_job<R>(0, (cx<R>*)dA->p, m, n, eps, chi, true);
+  run_jobs<R>(&j, 1);
+  read_info(1);
+  const int64_t k = E.h_info[0];
+  *rank = k;
+  *disc = E.h_disc[0];
+  Buf dU = alloc((size_t)(m * k) * sizeof(cx<R>)), dV = alloc((size_t)(k * n) * sizeof(cx<R>));
+  emit<R>(j, k, (cx<R>*)dU->p, false, (cx<R>*)dV->p, false);
+  std::vector<R> sg(k);
+  ck(cudaMemcpyAsync(sg.data(), j.sig, k * sizeof(R), cudaMemcpyDeviceToHost, E.stream), "d2h");
+  sync();
+  download<R>((cx<R>*)dU->p, u, m * k);
+  sync();
+  download<R>((cx<R>*)dV->p, v, k * n);
+  sync();
+  for (int64_t i = 0; i < k; ++i) s[i] = (double)sg[i];
+}
+
+}  // namespace mb
+
+// =============================================================================
+// extern "C" boundary
+// =============================================================================
+
+using namespace mb;
+
+#define MB_TRY(body)                        \
+  try {                                     \
+    body;                                   \
+  } catch (const MbError& e) {              \
+    g_err = e.what();                       \
+    return e.code;                          \
+  } catch (const std::exception& e) {       \
+    g_err = e.what();                       \
+    return MB_ERR_ARG;                      \
+  }
+
+#define MB_TRY_PTR(body)                    \
+  try {                                     \
+    body;                                   \
+  } catch (const std::exception& e) {       \
+    g_err = e.what();                       \
+    return nullptr;                         \
+  }
+
+#define DISPATCH(dt, FN, ...) \
+  ((dt) == MB_C64 ? FN<float>(__VA_ARGS__) : FN<double>(__VA_ARGS__))
+
+static void ensure_ready() {
+  if (!E.ready) {
+    if (mb_init(0) != 0) throw MbError(MB_ERR_CUDA, g_err);
+  }
+}
+
+extern "C" {
+
+const char* mb_last_error(void) { return g_err.c_str(); }
+
+int mb_version(void) { return 1; }
+
+int mb_init(int device) {
+  MB_TRY({
+    if (E.ready && E.device == device) return 0;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaMemPool_t pool;
+    ck(cudaDeviceGetDefaultMemPool(&pool, device), "mempool");
+    uint64_t thr = std::numeric_limits<uint64_t>::max();
+    ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+    ck(cudaMallocHost(&E.h_info, sizeof(int64_t) * 3 * Engine::kSlots), "pinned");
+    ck(cudaMallocHost(&E.h_disc, sizeof(double) * Engine::kSlots), "pinned");
+    ck(cudaMallocHost(&E.h_scalar, sizeof(double) * 4), "pinned");
+    ck(cudaMallocHost(&E.h_flag, sizeof(int) * 4), "pinned");
+    E.device = device;
+    E.d_info = alloc(sizeof(int64_t) * 3 * Engine::kSlots);
+    E.d_disc = alloc(sizeof(double) * Engine::kSlots);
+    E.d_flag = alloc(sizeof(int) * 4);
+    E.d_scalar = alloc(sizeof(double) * 4);
+    E.ready = true;
+    ck(cudaStreamSynchronize(E.stream), "init sync");
+    return 0;
+  });
+}
+
+void* mb_stream(void) { return (void*)E.stream; }
+
+int mb_synchronize(void) {
+  MB_TRY({
+    ensure_ready();
+    ck(cudaStreamSynchronize(E.stream), "sync");
+    return 0;
+  });
+}
+
+long long mb_launch_count(void) { return launch_count(); }
+
+int mb_profile_begin(void) {
+  MB_TRY({
+    ensure_ready();
+    for (auto& r : E.recs) {
+      E.pool.push_back(r.a);
+      E.pool.push_back(r.b);
+    }
+    E.recs.clear();
+    E.prof = true;
+    return 0;
+  });
+}
+
+int mb_profile_end(double* ms, long long* launches, double* flops) {
+  MB_TRY({
+    ensure_ready();
+    ck(cudaStreamSynchronize(E.stream), "profile sync");
+    for (int i = 0; i < 6; ++i) {
+      ms[i] = 0;
+      launches[i] = 0;
+      flops[i] = 0;
+    }
+    for (auto& r : E.recs) {
+      float t = 0;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      ms[r.cls] += t;
+      launches[r.cls] += 1;
+      flops[r.cls] += r.flops;
+      E.pool.push_back(r.a);
+      E.pool.push_back(r.b);
+    }
+    E.recs.clear();
+    E.prof = false;
+    return 0;
+  });
+}
+
+int mb_counters(long long* out6) {
+  for (int i = 0; i < 6; ++i) out6[i] = E.counters[i];
+  return 0;
+}
+
+mb_chain* mb_identity_mpo(int n, int dtype) {
+  MB_TRY_PTR({
+    ensure_ready();
+    require(n >= 1, "need at least one site");
+    require(dtype == MB_C128 || dtype == MB_C64, "bad dtype");
+    std::vector<int64_t> bonds(n + 1, 1);
+    std::vector<double> data(8 * n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      data[8 * i + 0] = 1.0;  // (t=0,b=0)
+      data[8 * i + 6] = 1.0;  // (t=1,b=1)
+    }
+    return DISPATCH(dtype, from_host, n, 4, dtype, bonds.data(), data.data(), 0.0, -1);
+  });
+}
+
+mb_chain* mb_chain_from_host(int n, int d, int dtype, const int64_t* bonds, const double* data,
+                             double log_norm, int center) {
+  MB_TRY_PTR({
+    ensure_ready();
+    require(n >= 1 && (d == 2 || d == 4), "bad chain shape");
+    require(bonds[0] == 1 && bonds[n] == 1, "boundary bonds must have extent 1");
+    require(center >= -1 && center < n, "bad center");
+    return DISPATCH(dtype, from_host, n, d, dtype, bonds, data, log_norm, center);
+  });
+}
+
+mb_chain* mb_chain_clone(const mb_chain* c) {
+  MB_TRY_PTR({ return new mb_chain(*c); });
+}
+
+void mb_chain_free(mb_chain* c) { delete c; }
+
+int mb_chain_info(const mb_chain* c, int* n, int* d, int* dtype, double* log_norm, int* center) {
+  *n = c->n;
+  *d = c->d;
+  *dtype = c->dtype;
+  *log_norm = c->log_norm;
+  *center = c->center;
+  return 0;
+}
+
+int mb_chain_bonds(const mb_chain* c, int64_t* bonds) {
+  for (int i = 0; i < c->n; ++i) bonds[i] = c->s[i].l;
+  bonds[c->n] = c->s[c->n - 1].r;
+  return 0;
+}
+
+int64_t mb_total_elements(const mb_chain* c) {
+  int64_t t = 0;
+  for (auto& s : c->s) t += s.l * c->d * s.r;
+  return t;
+}
+
+int mb_chain_to_host(const mb_chain* c, double* data) {
+  MB_TRY({
+    ensure_ready();
+    if (c->dtype == MB_C64) to_host<float>(*c, data);
+    else to_host<double>(*c, data);
+    return 0;
+  });
+}
+
+int mb_absorb_1q(mb_chain* c, int q, const double* u2, int side) {
+  MB_TRY({
+    if (c->dtype == MB_C64) absorb_1q<float>(*c, q, u2, side);
+    else absorb_1q<double>(*c, q, u2, side);
+    return 0;
+  });
+}
+
+int mb_absorb_2q(mb_chain* c, int lo, const double* g4, int side, double eps, int64_t chi) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    if (c->dtype == MB_C64) absorb_2q<float>(*c, lo, g4, side, eps, chi);
+    else absorb_2q<double>(*c, lo, g4, side, eps, chi);
+    return 0;
+  });
+}
+
+int mb_move_center(mb_chain* c, int target) {
+  MB_TRY({
+    if (c->dtype == MB_C64) move_center<float>(*c, target);
+    else move_center<double>(*c, target);
+    return 0;
+  });
+}
+
+int mb_pair_swap(mb_chain* c, int bond, int top, int bottom, double eps, int64_t chi, int recenter) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    if (c->dtype == MB_C64) pair_swap<float>(*c, bond, top != 0, bottom != 0, eps, chi, recenter != 0);
+    else pair_swap<double>(*c, bond, top != 0, bottom != 0, eps, chi, recenter != 0);
+    return 0;
+  });
+}
+
+int mb_swap_extents(mb_chain* c, int bond, int ns, const int* sides, double eps, int64_t chi,
+                    int64_t* out) {
+  MB_TRY({
+    if (c->dtype == MB_C64) swap_extents<float>(*c, bond, ns, sides, eps, chi, out);
+    else swap_extents<double>(*c, bond, ns, sides, eps, chi, out);
+    return 0;
+  });
+}
+
+int mb_compress(mb_chain* c, double eps, int64_t chi) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    if (c->dtype == MB_C64) compress<float>(*c, eps, chi);
+    else compress<double>(*c, eps, chi);
+    return 0;
+  });
+}
+
+int mb_frobenius_norm(const mb_chain* c, double* out) {
+  MB_TRY({
+    *out = c->dtype == MB_C64 ? frob<float>(*c) : frob<double>(*c);
+    return 0;
+  });
+}
+
+mb_chain* mb_apply_to_zero(const mb_chain* c, double eps, int64_t chi) {
+  MB_TRY_PTR({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    return c->dtype == MB_C64 ? apply_to_zero<float>(*c, eps, chi) : apply_to_zero<double>(*c, eps, chi);
+  });
+}
+
+int mb_peak(const mb_chain* psi, uint8_t* bits, double* probs) {
+  MB_TRY({
+    if (psi->dtype == MB_C64) peak<float>(*psi, bits, probs);
+    else peak<double>(*psi, bits, probs);
+    return 0;
+  });
+}
+
+int mb_sample(const mb_chain* psi, int64_t shots, const double* uniforms, uint8_t* bits) {
+  MB_TRY({
+    if (psi->dtype == MB_C64) sample<float>(*psi, shots, uniforms, bits);
+    else sample<double>(*psi, shots, uniforms, bits);
+    return 0;
+  });
+}
+
+int mb_svd_truncate(const double* a, int64_t m, int64_t n, int dtype, double eps, int64_t chi,
+                    double* u, double* s, double* v, int64_t* rank, double* disc) {
+  MB_TRY({
+    ensure_ready();
+    require(m >= 1 && n >= 1, "empty matrix");
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    if (dtype == MB_C64) svd_host<float>(a, m, n, eps, chi, u, s, v, rank, disc);
+    else svd_host<double>(a, m, n, eps, chi, u, s, v, rank, disc);
+    return 0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,943 @@
+// CUDA kernels of the B200 middle-MPO engine (sm_100a).
+//
+//  * k_gemm          : tiled complex GEMM (pair blob, R-carry, L-carry).
+//  * k_gate2/k_gate1 : 4x4 / 2x2 gate application on blob / site legs
+//                      (reference chains.py:190-216).
+//  * k_svd_small     : whole-matrix one-CTA block Jacobi SVD with in-kernel
+//                      sort and truncation rank (tensor.py:84-136) — batched.
+//  * k_jacobi_pair   : one block-pair step of the multi-CTA block Jacobi SVD.
+//  * k_emit          : writes truncated factors straight into site layout.
+//  * k_peak          : single-CTA sequential MPS marginal sweep.
+#include "mb_kernels.cuh"
+
+#include <atomic>
+#include <cstdio>
+#include <vector>
+
+namespace mb {
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+
+#define MB_LAUNCH_CHECK()                                                              \
+  do {                                                                                 \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                \
+    cudaError_t e_ = cudaGetLastError();                                               \
+    if (e_ != cudaSuccess) {                                                           \
+      fprintf(stderr, "mirrorbreak_b200 kernel launch failed: %s (%s:%d)\n",            \
+              cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+    }                                                                                  \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// GEMM: C[M x N] = op(A) B, row-major; op(A) = A (M x K) or A^H (A is K x M).
+// ---------------------------------------------------------------------------
+
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+template <typename R, bool CT>
+__global__ void __launch_bounds__(256) k_gemm(int64_t M, int64_t N, int64_t K,
+                                              const cx<R>* __restrict__ A, int64_t lda,
+                                              const cx<R>* __restrict__ B, int64_t ldb,
+                                              cx<R>* __restrict__ C, int64_t ldc) {
+  __shared__ cx<R> As[GBK][GBM + 1];
+  __shared__ cx<R> Bs[GBK][GBN + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * GBM, n0 = (int64_t)blockIdx.x * GBN;
+  cx<R> acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = mk<R>(0, 0);
+  const cx<R> zero = mk<R>(0, 0);
+  for (int64_t k0 = 0; k0 < K; k0 += GBK) {
+#pragma unroll
+    for (int t = 0; t < (GBM * GBK) / 256; ++t) {
+      int e = tid + 256 * t;
+      if (!CT) {
+        int mm = e / GBK, kk = e % GBK;
+        int64_t gm = m0 + mm, gk = k0 + kk;
+        As[kk][mm] = (gm < M && gk < K) ? A[gm * lda + gk] : zero;
+      } else {
+        int kk = e / GBM, mm = e % GBM;
+        int64_t gm = m0 + mm, gk = k0 + kk;
+        As[kk][mm] = (gm < M && gk < K) ? cconj(A[gk * lda + gm]) : zero;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < (GBN * GBK) / 256; ++t) {
+      int e = tid + 256 * t;
+      int kk = e / GBN, nn = e % GBN;
+      int64_t gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < K && gn < N) ? B[gk * ldb + gn] : zero;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < GBK; ++kk) {
+      cx<R> a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cfma(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t gn = n0 + tx + 16 * j;
+      if (gn < N) C[gm * ldc + gn] = acc[i][j];
+    }
+  }
+}
+
+template <typename R>
+void launch_gemm(bool conjTransA, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64_t lda,
+                 const cx<R>* B, int64_t ldb, cx<R>* C, int64_t ldc, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid((unsigned)cdiv(N, GBN), (unsigned)cdiv(M, GBM));
+  if (conjTransA)
+    k_gemm<R, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  else
+    k_gemm<R, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  MB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Gate application. Blob theta has axes (l, t1, b1, t2, b2, r); the 4x4 gate
+// g16[(o_lo*2+o_hi)*4 + (i_lo*2+i_hi)] is ordered by site index (chains.py:148).
+//  left : theta'[l,x,b1,y,b2,r] = sum_{t,u} G[x,y,t,u] theta[l,t,b1,u,b2,r]
+//  right: theta'[l,t1,x,t2,y,r] = sum_{b,a} theta[l,t1,b,t2,a,r] G[b,a,x,y]
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void k_gate2(cx<R>* __restrict__ th, const Gate4<R> G, int64_t l, int64_t r,
+                        bool left) {
+  const cx<R>* g = G.g;
+  int64_t total = l * 4 * r;  // (l, fixed pair of 2-valued legs, r)
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rr = e % r;
+    int64_t rest = e / r;
+    int f2 = rest % 2;  // second untouched leg
+    int f1 = (rest / 2) % 2;
+    int64_t ll = rest / 4;
+    // strides of (t1, b1, t2, b2) in the blob
+    const int64_t sb2 = r, st2 = 2 * r, sb1 = 4 * r, st1 = 8 * r;
+    int64_t base = ll * 16 * r + rr;
+    int64_t s_hi, s_lo;  // strides of the two legs the gate touches (lo-site, hi-site)
+    if (left) {
+      base += f1 * sb1 + f2 * sb2;
+      s_lo = st1;
+      s_hi = st2;
+    } else {
+      base += f1 * st1 + f2 * st2;
+      s_lo = sb1;
+      s_hi = sb2;
+    }
+    cx<R> v[4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) v[a * 2 + b] = th[base + a * s_lo + b * s_hi];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      cx<R> acc = mk<R>(0, 0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // left: out o = (x,y) row of G; right: out o = (x,y) column of G
+        cx<R> gg = left ? g[o * 4 + i] : g[i * 4 + o];
+        cfma(acc, gg, v[i]);
+      }
+      th[base + (o >> 1) * s_lo + (o & 1) * s_hi] = acc;
+    }
+  }
+}
+
+template <typename R>
+void launch_gate2(cx<R>* theta, const Gate4<R>& g, int64_t l, int64_t r, bool left,
+                  cudaStream_t s) {
+  int64_t total = l * 4 * r;
+  int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  k_gate2<R><<<blocks, 256, 0, s>>>(theta, g, l, r, left);
+  MB_LAUNCH_CHECK();
+}
+
+// site (l, t, b, r). left: new[l,t,b,r] = sum_k u[t,k] S[l,k,b,r];
+// right: new[l,t,b,r] = sum_k S[l,t,k,r] u[k,b]   (chains.py:190-201)
+template <typename R>
+__global__ void k_gate1(const cx<R>* __restrict__ src, cx<R>* __restrict__ st, const Gate2<R> U,
+                        int64_t l, int64_t r, bool left) {
+  const cx<R>* u = U.g;
+  int64_t total = l * 2 * r;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rr = e % r;
+    int f = (e / r) % 2;
+    int64_t ll = e / (2 * r);
+    int64_t base = ll * 4 * r + rr;
+    int64_t sl = left ? 2 * r : r;       // stride of the contracted leg
+    int64_t sf = left ? r : 2 * r;       // stride of the untouched leg
+    base += f * sf;
+    cx<R> v0 = src[base], v1 = src[base + sl];
+    cx<R> o0 = mk<R>(0, 0), o1 = mk<R>(0, 0);
+    if (left) {
+      cfma(o0, u[0], v0); cfma(o0, u[1], v1);
+      cfma(o1, u[2], v0); cfma(o1, u[3], v1);
+    } else {
+      cfma(o0, v0, u[0]); cfma(o0, v1, u[2]);
+      cfma(o1, v0, u[1]); cfma(o1, v1, u[3]);
+    }
+    st[base] = o0;
+    st[base + sl] = o1;
+  }
+}
+
+template <typename R>
+void launch_gate1(const cx<R>* src, cx<R>* dst, const Gate2<R>& u, int64_t l, int64_t r, bool left,
+                  cudaStream_t s) {
+  int64_t total = l * 2 * r;
+  int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  k_gate1<R><<<blocks, 256, 0, s>>>(src, dst, u, l, r, left);
+  MB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Block Jacobi machinery shared by the small and large SVD paths.
+// ---------------------------------------------------------------------------
+
+constexpr int TQ = 32;  // rows of X staged per chunk
+
+template <typename R>
+__device__ __forceinline__ double rel_tol(int64_t q) {
+  double s = sqrt((double)(q > 1 ? q : 1));
+  return (s > 8.0 ? s : 8.0) * 4.0 * Eps<R>::u;
+}
+
+// Tournament (circle method) pairing for NP even: round rnd, pair i.
+__device__ __forceinline__ void tournament(int NP, int rnd, int i, int& a, int& b) {
+  a = (i == 0) ? 0 : ((i - 1 + rnd) % (NP - 1)) + 1;
+  int j = NP - 1 - i;
+  b = ((j - 1 + rnd) % (NP - 1)) + 1;
+}
+
+template <typename R, int W2>
+struct PairSmem {
+  cx<R> xs[W2][TQ + 1];
+  cx<R> h[W2][W2 + 1];
+  cx<R> w[W2][W2 + 1];
+  R cs[W2 / 2];
+  R sn[W2 / 2];
+  cx<R> ph[W2 / 2];
+  int pj[W2 / 2], pk[W2 / 2];
+  int col[W2];
+  int flag;
+};
+
+// Gram of the selected columns: h[a][b] = x_a^H x_b over all q rows.
+template <typename R, int W2>
+__device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64_t q) {
+  constexpr int TM = W2 / 16;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  cx<R> acc[TM][TM];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TM; ++j) acc[i][j] = mk<R>(0, 0);
+  for (int64_t i0 = 0; i0 < q; i0 += TQ) {
+    for (int e = tid; e < W2 * TQ; e += blockDim.x) {
+      int c = e / TQ, t = e % TQ;
+      int gc = S.col[c];
+      S.xs[c][t] = (gc >= 0 && i0 + t < q) ? X[(int64_t)gc * q + i0 + t] : mk<R>(0, 0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int t = 0; t < TQ; ++t) {
+      cx<R> a[TM], b[TM];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = S.xs[ty + 16 * i][t];
+#pragma unroll
+      for (int j = 0; j < TM; ++j) b[j] = S.xs[tx + 16 * j][t];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TM; ++j) cfmac(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TM; ++j) S.h[ty + 16 * i][tx + 16 * j] = acc[i][j];
+  __syncthreads();
+}
+
+// Is the Gram off-diagonal above tolerance (relative to the diagonal)?
+template <typename R, int W2>
+__device__ bool pair_offdiag(PairSmem<R, W2>& S, double tol) {
+  if (threadIdx.x == 0) S.flag = 0;
+  __syncthreads();
+  double t2 = tol * tol;
+  for (int e = threadIdx.x; e < W2 * W2; e += blockDim.x) {
+    int a = e / W2, b = e % W2;
+    if (a >= b) continue;
+    double haa = S.h[a][a].x, hbb = S.h[b][b].x;
+    double g2 = (double)cabs2(S.h[a][b]);
+    if (haa > 0 && hbb > 0 && g2 > t2 * haa * hbb) S.flag = 1;
+  }
+  __syncthreads();
+  return S.flag != 0;
+}
+
+// Two-sided cyclic Jacobi on the Hermitian h; accumulates the rotation in w.
+template <typename R, int W2>
+__device__ void pair_evd(PairSmem<R, W2>& S, double tol) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < W2 * W2; e += blockDim.x) {
+    int a = e / W2, b = e % W2;
+    S.w[a][b] = mk<R>(a == b ? 1 : 0, 0);
+  }
+  __syncthreads();
+  const double t2 = tol * tol;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    if (tid == 0) S.flag = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < W2 - 1; ++rnd) {
+      if (tid < W2 / 2) {
+        int j, k;
+        tournament(W2, rnd, tid, j, k);
+        if (j > k) { int t = j; j = k; k = t; }
+        S.pj[tid] = j;
+        S.pk[tid] = k;
+        double a = S.h[j][j].x, b = S.h[k][k].x;
+        cx<R> g = S.h[j][k];
+        double ga2 = (double)cabs2(g);
+        if (a > 0 && b > 0 && ga2 > t2 * a * b) {
+          double ga = sqrt(ga2);
+          double zeta = (b - a) / (2.0 * ga);
+          double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double c = 1.0 / sqrt(1.0 + t * t);
+          S.cs[tid] = (R)c;
+          S.sn[tid] = (R)(c * t);
+          S.ph[tid] = mk<R>((R)(g.x / ga), (R)(-g.y / ga));  // e^{-i phi}
+          S.flag = 1;
+        } else {
+          S.cs[tid] = 1;
+          S.sn[tid] = 0;
+          S.ph[tid] = mk<R>(1, 0);
+        }
+      }
+      __syncthreads();
+      // rows: H <- J^H H
+      for (int e = tid; e < (W2 / 2) * W2; e += blockDim.x) {
+        int p = e / W2, c = e % W2;
+        R cc = S.cs[p], ss = S.sn[p];
+        if (ss == 0) continue;
+        int j = S.pj[p], k = S.pk[p];
+        cx<R> ep = cconj(S.ph[p]);
+        cx<R> hj = S.h[j][c], hk = S.h[k][c];
+        cx<R> ek = cmul(ep, hk);
+        S.h[j][c] = csub(cscale(hj, cc), cscale(ek, ss));
+        S.h[k][c] = cadd(cscale(hj, ss), cscale(ek, cc));
+      }
+      __syncthreads();
+      // columns: H <- H J, W <- W J
+      for (int e = tid; e < (W2 / 2) * W2 * 2; e += blockDim.x) {
+        int which = e / ((W2 / 2) * W2);
+        int e2 = e % ((W2 / 2) * W2);
+        int p = e2 / W2, rr = e2 % W2;
+        R cc = S.cs[p], ss = S.sn[p];
+        if (ss == 0) continue;
+        int j = S.pj[p], k = S.pk[p];
+        cx<R> ep = S.ph[p];
+        cx<R>(*M)[W2 + 1] = which ? S.w : S.h;
+        cx<R> mj = M[rr][j], mk_ = M[rr][k];
+        cx<R> ek = cmul(mk_, ep);
+        M[rr][j] = csub(cscale(mj, cc), cscale(ek, ss));
+        M[rr][k] = cadd(cscale(mj, ss), cscale(ek, cc));
+      }
+      __syncthreads();
+    }
+    if (S.flag == 0) break;
+    __syncthreads();
+  }
+}
+
+// Y[:, cols] <- Y[:, cols] W for a column-major matrix with column length len.
+template <typename R, int W2>
+__device__ void pair_apply(PairSmem<R, W2>& S, cx<R>* __restrict__ Y, int64_t len) {
+  const int tid = threadIdx.x;
+  for (int64_t i0 = 0; i0 < len; i0 += TQ) {
+    for (int e = tid; e < W2 * TQ; e += blockDim.x) {
+      int c = e / TQ, t = e % TQ;
+      int gc = S.col[c];
+      S.xs[c][t] = (gc >= 0 && i0 + t < len) ? Y[(int64_t)gc * len + i0 + t] : mk<R>(0, 0);
+    }
+    __syncthreads();
+    for (int e = tid; e < W2 * TQ; e += blockDim.x) {
+      int c = e / TQ, t = e % TQ;
+      int gc = S.col[c];
+      if (gc < 0 || i0 + t >= len) continue;
+      cx<R> acc = mk<R>(0, 0);
+#pragma unroll 8
+      for (int c2 = 0; c2 < W2; ++c2) cfma(acc, S.xs[c2][t], S.w[c2][c]);
+      Y[(int64_t)gc * len + i0 + t] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Truncation rank on a descending spectrum (tensor.py:119-136). Serial; run
+// by one thread. Writes rank and discarded weight.
+template <typename R>
+__device__ void rank_rule(const R* sig, int p, double eps, int64_t chi, int64_t* rank_out,
+                          double* disc_out) {
+  double total = 0;
+  for (int k = 0; k < p; ++k) total += (double)sig[k] * (double)sig[k];
+  double budget = eps * eps * total;
+  // suffix sums from the end, as numpy's reversed cumsum
+  int r = p;
+  double tail = 0;
+  // find smallest k>=1 with tail(k) <= budget: scan k from p down to 1
+  for (int k = p; k >= 1; --k) {
+    // tail currently = sum_{j>=k} w_j
+    if (tail <= budget) r = k;
+    else break;
+    tail += (double)sig[k - 1] * (double)sig[k - 1];
+  }
+  double edge = sig[r - 1];
+  while (r < p && (double)sig[r] >= edge - 1e-12) ++r;
+  int64_t rk = r < chi ? r : chi;
+  double disc = 0;
+  for (int k = (int)rk; k < p; ++k) disc += (double)sig[k] * (double)sig[k];
+  *rank_out = rk;
+  *disc_out = total > 0 ? disc / total : 0.0;
+}
+
+// Initialize X (column-major working matrix) and V = I for one job.
+template <typename R>
+__device__ void job_init(const SvdJob<R>& J, int64_t p, int64_t q) {
+  const int64_t m = J.m, n = J.n;
+  for (int64_t e = threadIdx.x; e < p * q; e += blockDim.x) {
+    int64_t j = e / q, i = e % q;  // column j, row i of X
+    cx<R> v;
+    if (m >= n) v = J.A[i * n + j];              // X = A^T
+    else v = cconj(J.A[j * n + i]);              // X = A^H
+    J.X[e] = v;
+  }
+  if (J.V) {
+    for (int64_t e = threadIdx.x; e < p * p; e += blockDim.x) {
+      int64_t j = e / p, i = e % p;
+      J.V[e] = mk<R>(i == j ? 1 : 0, 0);
+    }
+  }
+  __syncthreads();
+}
+
+template <typename R>
+struct JobPack {
+  SvdJob<R> j[kPackJobs];
+};
+
+template <typename R, int W2>
+__global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  const SvdJob<R> J = pack.j[blockIdx.x];
+  const int64_t p = J.m < J.n ? J.m : J.n;
+  const int64_t q = J.m < J.n ? J.n : J.m;
+  if (p > W2) return;
+  if (J.A) job_init(J, p, q);
+  for (int c = threadIdx.x; c < W2; c += blockDim.x) S.col[c] = c < p ? c : -1;
+  __syncthreads();
+  const double tol = rel_tol<R>(q);
+  int it = 0, converged = 0;
+  for (; it < 16; ++it) {
+    pair_gram<R, W2>(S, J.X, q);
+    if (!pair_offdiag<R, W2>(S, tol)) { converged = 1; break; }
+    pair_evd<R, W2>(S, tol);
+    pair_apply<R, W2>(S, J.X, q);
+    if (J.V) pair_apply<R, W2>(S, J.V, p);
+  }
+  if (!converged) pair_gram<R, W2>(S, J.X, q);
+  // column norms from the final Gram diagonal; rank-by-count sort (desc, stable)
+  __shared__ R sg[W2];
+  for (int c = threadIdx.x; c < W2; c += blockDim.x) {
+    R d = c < p ? S.h[c][c].x : (R)0;
+    sg[c] = d > 0 ? sqrt(d) : (R)0;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    R v = sg[c];
+    int pos = 0;
+    for (int c2 = 0; c2 < p; ++c2) {
+      R u = sg[c2];
+      pos += (u > v) || (u == v && c2 < c);
+    }
+    J.sig[pos] = v;
+    J.perm[pos] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // re-read sorted values (global, written by this block)
+    __threadfence_block();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    rank_rule<R>(J.sig, (int)p, J.eps, J.chi, &J.info[0], J.disc);
+    J.info[1] = converged ? 0 : 1;
+    J.info[2] = it;
+  }
+}
+
+template <typename R>
+void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t s) {
+  static bool attr32 = false, attr64 = false;
+  for (int b = 0; b < njobs; b += kPackJobs) {
+    JobPack<R> pack;
+    int cnt = njobs - b < kPackJobs ? njobs - b : kPackJobs;
+    for (int i = 0; i < cnt; ++i) pack.j[i] = jobs[b + i];
+    if (max_p <= 32) {
+      size_t sm = sizeof(PairSmem<R, 32>);
+      if (!attr32) {
+        cudaFuncSetAttribute(k_svd_small<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr32 = true;
+      }
+      k_svd_small<R, 32><<<cnt, 256, sm, s>>>(pack);
+    } else {
+      size_t sm = sizeof(PairSmem<R, 64>);
+      if (!attr64) {
+        cudaFuncSetAttribute(k_svd_small<R, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr64 = true;
+      }
+      k_svd_small<R, 64><<<cnt, 256, sm, s>>>(pack);
+    }
+    MB_LAUNCH_CHECK();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Large path: block one-sided Jacobi, blocks of w = W2/2 columns, one CTA per
+// block pair per tournament round.
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void k_init_large(const cx<R>* __restrict__ A, cx<R>* __restrict__ X,
+                             cx<R>* __restrict__ V, int64_t m, int64_t n) {
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  const int64_t tot = p * q + p * p;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < p * q) {
+      int64_t j = e / q, i = e % q;
+      X[e] = (m >= n) ? A[i * n + j] : cconj(A[j * n + i]);
+    } else if (V) {
+      int64_t f = e - p * q;
+      int64_t j = f / p, i = f % p;
+      V[f] = mk<R>(i == j ? 1 : 0, 0);
+    }
+  }
+}
+
+template <typename R, int W2>
+__global__ void __launch_bounds__(256) k_jacobi_pair(cx<R>* __restrict__ X, cx<R>* __restrict__ V,
+                                                     int64_t p, int64_t q, int nb, int NB, int rnd,
+                                                     int* __restrict__ flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  constexpr int w = W2 / 2;
+  int a, b;
+  tournament(NB, rnd, blockIdx.x, a, b);
+  for (int c = threadIdx.x; c < W2; c += blockDim.x) {
+    int blk = c < w ? a : b;
+    int64_t gc = (int64_t)blk * w + (c % w);
+    S.col[c] = (blk < nb && gc < p) ? (int)gc : -1;
+  }
+  __syncthreads();
+  const double tol = rel_tol<R>(q);
+  pair_gram<R, W2>(S, X, q);
+  if (!pair_offdiag<R, W2>(S, tol)) return;
+  pair_evd<R, W2>(S, tol);
+  pair_apply<R, W2>(S, X, q);
+  if (V) pair_apply<R, W2>(S, V, p);
+  if (threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename R>
+__global__ void k_colnorms(const cx<R>* __restrict__ X, int64_t p, int64_t q, R* __restrict__ out) {
+  __shared__ double red[256];
+  for (int64_t j = blockIdx.x; j < p; j += gridDim.x) {
+    double acc = 0;
+    for (int64_t i = threadIdx.x; i < q; i += blockDim.x) acc += (double)cabs2(X[j * q + i]);
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j] = (R)sqrt(red[0]);
+    __syncthreads();
+  }
+}
+
+template <typename R>
+__global__ void k_sort_desc(const R* __restrict__ vals, int64_t p, R* __restrict__ sig,
+                            int* __restrict__ perm) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < p;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    R v = vals[c];
+    int64_t pos = 0;
+    for (int64_t c2 = 0; c2 < p; ++c2) {
+      R u = vals[c2];
+      pos += (u > v) || (u == v && c2 < c);
+    }
+    sig[pos] = v;
+    perm[pos] = (int)c;
+  }
+}
+
+template <typename R>
+__global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    rank_rule<R>(J.sig, (int)p, J.eps, J.chi, &J.info[0], J.disc);
+    J.info[1] = conv ? 0 : 1;
+    J.info[2] = sweeps;
+  }
+}
+
+template <typename R>
+void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, cudaStream_t s) {
+  constexpr int W2 = 64;
+  constexpr int w = W2 / 2;
+  const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
+  if (J.A) {
+    int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
+    k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n);
+    MB_LAUNCH_CHECK();
+  }
+  const int nb = (int)cdiv(p, w);
+  const int NB = nb + (nb & 1);
+  size_t sm = sizeof(PairSmem<R, W2>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_jacobi_pair<R, W2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  int sweeps = 0, conv = 0;
+  for (; sweeps < 40; ++sweeps) {
+    cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
+    for (int rnd = 0; rnd < NB - 1; ++rnd) {
+      k_jacobi_pair<R, W2><<<NB / 2, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd, flag_dev);
+      MB_LAUNCH_CHECK();
+    }
+    cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (*flag_host == 0) { conv = 1; break; }
+  }
+  // column norms into sig[p:2p] (the engine sizes sig for 2p), then sort into sig[0:p]
+  k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(J.X, p, q, J.sig + p);
+  MB_LAUNCH_CHECK();
+  k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
+  MB_LAUNCH_CHECK();
+  k_rank<R><<<1, 32, 0, s>>>(J, p, conv, sweeps);
+  MB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Emit truncated factors.
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void k_emit(SvdJob<R> J, int64_t k, cx<R>* __restrict__ U, bool scaleU,
+                       cx<R>* __restrict__ Vo, bool scaleV) {
+  const int64_t m = J.m, n = J.n;
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  const bool tall = m >= n;
+  const int64_t nu = U ? m * k : 0, nv = Vo ? k * n : 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nu + nv;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < nu) {
+      int64_t i = e / k, kk = e % k;
+      int src = J.perm[kk];
+      R sg = J.sig[kk];
+      cx<R> v;
+      if (tall) {
+        v = J.X[(int64_t)src * q + i];
+        if (!scaleU) v = sg > 0 ? cscale(v, (R)1 / sg) : mk<R>(0, 0);
+      } else {
+        v = J.V[(int64_t)src * p + i];
+        if (scaleU) v = cscale(v, sg);
+      }
+      U[e] = v;
+    } else {
+      int64_t f = e - nu;
+      int64_t kk = f / n, c = f % n;
+      int src = J.perm[kk];
+      R sg = J.sig[kk];
+      cx<R> v;
+      if (tall) {
+        v = cconj(J.V[(int64_t)src * p + c]);
+        if (scaleV) v = cscale(v, sg);
+      } else {
+        v = cconj(J.X[(int64_t)src * q + c]);
+        if (!scaleV) v = sg > 0 ? cscale(v, (R)1 / sg) : mk<R>(0, 0);
+      }
+      Vo[f] = v;
+    }
+  }
+}
+
+template <typename R>
+void launch_emit(const SvdJob<R>& J, int64_t k, cx<R>* Uout, bool scaleU, cx<R>* Vout,
+                 bool scaleV, cudaStream_t s) {
+  int64_t tot = (Uout ? J.m * k : 0) + (Vout ? k * J.n : 0);
+  if (tot == 0) return;
+  int blocks = (int)std::min<int64_t>(cdiv(tot, 256), 148 * 16);
+  k_emit<R><<<blocks, 256, 0, s>>>(J, k, Uout, scaleU, Vout, scaleV);
+  MB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Small utilities.
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void k_identity(cx<R>* out, int64_t m) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = mk<R>((e / m) == (e % m) ? 1 : 0, 0);
+}
+
+template <typename R>
+void launch_identity(cx<R>* out, int64_t m, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(m * m, 256), 148 * 8);
+  k_identity<R><<<blocks, 256, 0, s>>>(out, m);
+  MB_LAUNCH_CHECK();
+}
+
+template <typename R>
+__global__ void k_scale(cx<R>* buf, int64_t n, double f) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    buf[e] = cscale(buf[e], (R)f);
+}
+
+template <typename R>
+void launch_scale(cx<R>* buf, int64_t n, double f, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(n, 256), 148 * 8);
+  k_scale<R><<<blocks, 256, 0, s>>>(buf, n, f);
+  MB_LAUNCH_CHECK();
+}
+
+constexpr int kSumBlocks = 256;
+
+template <typename R>
+__global__ void k_sumsq_partial(const cx<R>* __restrict__ buf, int64_t n, double* partial) {
+  __shared__ double red[256];
+  double acc = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    acc += (double)cabs2(buf[e]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void k_sumsq_final(const double* partial, int nb, double* out) {
+  __shared__ double red[256];
+  red[threadIdx.x] = threadIdx.x < nb ? partial[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+template <typename R>
+void launch_sumsq(const cx<R>* buf, int64_t n, double* partial, double* out, cudaStream_t s) {
+  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(buf, n, partial);
+  MB_LAUNCH_CHECK();
+  k_sumsq_final<<<1, 256, 0, s>>>(partial, kSumBlocks, out);
+  MB_LAUNCH_CHECK();
+}
+
+template <typename R>
+__global__ void k_slice_b0(const cx<R>* __restrict__ mpo, cx<R>* __restrict__ mps, int64_t l,
+                           int64_t r) {
+  int64_t tot = l * 2 * r;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rr = e % r, t = (e / r) % 2, ll = e / (2 * r);
+    mps[e] = mpo[((ll * 2 + t) * 2 + 0) * r + rr];
+  }
+}
+
+template <typename R>
+void launch_slice_b0(const cx<R>* mpo, cx<R>* mps, int64_t l, int64_t r, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(l * 2 * r, 256), 148 * 8);
+  k_slice_b0<R><<<blocks, 256, 0, s>>>(mpo, mps, l, r);
+  MB_LAUNCH_CHECK();
+}
+
+template <typename R>
+__global__ void k_convert(const void* src, bool src_double, cx<R>* dst, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (src_double) {
+      const double* s = (const double*)src;
+      dst[e] = mk<R>((R)s[2 * e], (R)s[2 * e + 1]);
+    } else {
+      const float* s = (const float*)src;
+      dst[e] = mk<R>((R)s[2 * e], (R)s[2 * e + 1]);
+    }
+  }
+}
+
+template <typename R>
+void launch_convert(const void* src, bool src_double, cx<R>* dst, int64_t n, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(n, 256), 148 * 8);
+  k_convert<R><<<blocks, 256, 0, s>>>(src, src_double, dst, n);
+  MB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// Peak extraction: one CTA walks the right-canonical MPS left to right,
+// carrying the normalized conditional environment of the chosen prefix in
+// shared memory (dims[3*i..] = l, 2, r of site i).
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void __launch_bounds__(1024) k_peak(const cx<R>* const* __restrict__ sites,
+                                               const int64_t* __restrict__ dims, int nsites,
+                                               uint8_t* __restrict__ bits,
+                                               double* __restrict__ probs, cx<R>* scratch) {
+  int64_t maxb = dims[3 * nsites];  // appended by the host: max bond
+  cx<R>* env = scratch;             // maxb   (L2-resident; one CTA)
+  cx<R>* amp = scratch + maxb;      // 2 * maxb
+  __shared__ double red[2][32];
+  __shared__ double pr[2];
+  if (threadIdx.x == 0) env[0] = mk<R>(1, 0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int s = 0; s < nsites; ++s) {
+    const int64_t l = dims[3 * s], r = dims[3 * s + 2];
+    const cx<R>* S = sites[s];
+    double acc0 = 0, acc1 = 0;
+    for (int64_t e = threadIdx.x; e < 2 * r; e += blockDim.x) {
+      int pb = (int)(e / r);
+      int64_t c = e % r;
+      cx<R> a = mk<R>(0, 0);
+      for (int64_t k = 0; k < l; ++k) cfma(a, env[k], S[(k * 2 + pb) * r + c]);
+      amp[e] = a;
+      double w = (double)cabs2(a);
+      if (pb) acc1 += w; else acc0 += w;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      acc0 += __shfl_down_sync(0xffffffffu, acc0, o);
+      acc1 += __shfl_down_sync(0xffffffffu, acc1, o);
+    }
+    if (lane == 0) { red[0][wid] = acc0; red[1][wid] = acc1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double p0 = 0, p1 = 0;
+      for (int i = 0; i < nw; ++i) { p0 += red[0][i]; p1 += red[1][i]; }
+      int pick = p1 > p0 ? 1 : 0;
+      bits[s] = (uint8_t)pick;
+      double tot = p0 + p1;
+      probs[s] = tot > 0 ? (pick ? p1 : p0) / tot : 0.0;
+      pr[0] = pick;
+      pr[1] = pick ? p1 : p0;
+    }
+    __syncthreads();
+    const int pick = (int)pr[0];
+    const double inv = pr[1] > 0 ? 1.0 / sqrt(pr[1]) : 0.0;
+    for (int64_t c = threadIdx.x; c < r; c += blockDim.x) env[c] = cscale(amp[pick * r + c], (R)inv);
+    __syncthreads();
+  }
+}
+
+template <typename R>
+void launch_peak(const cx<R>* const* sites, const int64_t* dims, int nsites, int64_t maxbond,
+                 uint8_t* bits, double* probs, cx<R>* scratch, cudaStream_t s) {
+  (void)maxbond;
+  k_peak<R><<<1, 1024, 0, s>>>(sites, dims, nsites, bits, probs, scratch);
+  MB_LAUNCH_CHECK();
+}
+
+// Sampling step (chains.py:362-371): amp is (shots, 2, r).
+template <typename R>
+__global__ void k_sample_pick(const cx<R>* __restrict__ amp, int64_t shots, int64_t r,
+                              const double* __restrict__ uni, uint8_t* __restrict__ bits,
+                              int64_t bstride, cx<R>* __restrict__ env) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sh = warp; sh < shots; sh += nwarps) {
+    const cx<R>* a = amp + sh * 2 * r;
+    double p0 = 0, p1 = 0;
+    for (int64_t c = lane; c < r; c += 32) {
+      p0 += (double)cabs2(a[c]);
+      p1 += (double)cabs2(a[r + c]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+      p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+    }
+    double pone = p1 / (p0 + p1);
+    int pick = uni[sh] < pone ? 1 : 0;
+    if (lane == 0) bits[sh * bstride] = (uint8_t)pick;
+    double inv = 1.0 / sqrt(pick ? p1 : p0);
+    for (int64_t c = lane; c < r; c += 32) env[sh * r + c] = cscale(a[pick * r + c], (R)inv);
+  }
+}
+
+template <typename R>
+void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double* uniforms,
+                        uint8_t* bits_col, int64_t bit_stride, cx<R>* env_out, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(shots * 32, 256), 148 * 8);
+  k_sample_pick<R><<<blocks, 256, 0, s>>>(amp, shots, r, uniforms, bits_col, bit_stride, env_out);
+  MB_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// explicit instantiations
+// ---------------------------------------------------------------------------
+
+#define MB_INSTANTIATE(R)                                                                       \
+  template void launch_gemm<R>(bool, int64_t, int64_t, int64_t, const cx<R>*, int64_t,           \
+                               const cx<R>*, int64_t, cx<R>*, int64_t, cudaStream_t);          \
+  template void launch_gate2<R>(cx<R>*, const Gate4<R>&, int64_t, int64_t, bool, cudaStream_t);  \
+  template void launch_gate1<R>(const cx<R>*, cx<R>*, const Gate2<R>&, int64_t, int64_t, bool,   \
+                                cudaStream_t);                                                  \
+  template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
+  template void svd_large<R>(const SvdJob<R>&, int*, int*, cudaStream_t);                       \
+  template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
+                               cudaStream_t);                                                   \
+  template void launch_identity<R>(cx<R>*, int64_t, cudaStream_t);                              \
+  template void launch_scale<R>(cx<R>*, int64_t, double, cudaStream_t);                         \
+  template void launch_sumsq<R>(const cx<R>*, int64_t, double*, double*, cudaStream_t);         \
+  template void launch_slice_b0<R>(const cx<R>*, cx<R>*, int64_t, int64_t, cudaStream_t);       \
+  template void launch_convert<R>(const void*, bool, cx<R>*, int64_t, cudaStream_t);            \
+  template void launch_peak<R>(const cx<R>* const*, const int64_t*, int, int64_t, uint8_t*,      \
+                               double*, cx<R>*, cudaStream_t);                                  \
+  template void launch_sample_pick<R>(const cx<R>*, int64_t, int64_t, const double*, uint8_t*,   \
+                                      int64_t, cx<R>*, cudaStream_t);
+
+MB_INSTANTIATE(double)
+MB_INSTANTIATE(float)
+
+}  // namespace mb

@@ -1,0 +1,101 @@
+// Kernel launch interface for the middle-MPO engine (implemented in mb_kernels.cu).
+#pragma once
+
+#include "mb_common.cuh"
+
+namespace mb {
+
+// One truncated-SVD problem. A (m x n, row-major) is factored through the
+// column-major working matrix X (p = min(m,n) columns of length q = max(m,n))
+// and the accumulated rotation V (p x p, column-major):
+//   m >= n : X = A^T,  A = (X/sigma) diag(sigma) V^H
+//   m <  n : X = A^H,  A = V diag(sigma) (X/sigma)^H
+template <typename R>
+struct SvdJob {
+  const cx<R>* A;
+  cx<R>* X;
+  cx<R>* V;
+  R* sig;          // 2p: [0,p) sorted descending, [p,2p) scratch
+  int* perm;       // p, sorted slot -> source column
+  int64_t m, n;
+  double eps;      // relative cutoff (tensor.py:119)
+  int64_t chi;     // bond cap
+  int64_t* info;   // [0]=kept rank, [1]=not-converged flag, [2]=sweeps
+  double* disc;    // discarded weight
+};
+
+// Largest column count a single CTA factors on its own.
+constexpr int kSmallP = 64;
+// Jobs passed by value per batched small-SVD launch.
+constexpr int kPackJobs = 8;
+
+// Kernels launched by this library since load (the bench's gpu_launches).
+long long launch_count();
+
+template <typename R>
+void launch_gemm(bool conjTransA, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64_t lda,
+                 const cx<R>* B, int64_t ldb, cx<R>* C, int64_t ldc, cudaStream_t s);
+
+// Gate matrices travel by value in the kernel parameters.
+template <typename R>
+struct Gate4 {
+  cx<R> g[16];  // [(o_lo*2+o_hi)*4 + (i_lo*2+i_hi)]
+};
+template <typename R>
+struct Gate2 {
+  cx<R> g[4];  // row-major 2x2
+};
+
+template <typename R>
+void launch_gate2(cx<R>* theta, const Gate4<R>& g, int64_t l, int64_t r, bool left, cudaStream_t s);
+
+template <typename R>
+void launch_gate1(const cx<R>* src, cx<R>* dst, const Gate2<R>& u, int64_t l, int64_t r, bool left,
+                  cudaStream_t s);
+
+// Batched small SVDs (p <= kSmallP): init + Jacobi + sort + rank, one CTA per
+// job; `jobs` is a HOST array (passed to the kernel by value). V may be null
+// for values-only problems.
+template <typename R>
+void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t s);
+
+// Large SVD (p > kSmallP): host-driven block Jacobi sweeps.
+template <typename R>
+void svd_large(const SvdJob<R>& job, int* flag_dev, int* flag_host, cudaStream_t s);
+
+// Write truncated factors: Uout (m x k) = U[:, :k] (* sigma if scaleU),
+// Vout (k x n) = (sigma if scaleV *) Vh[:k, :]. Either pointer may be null.
+template <typename R>
+void launch_emit(const SvdJob<R>& job, int64_t k, cx<R>* Uout, bool scaleU, cx<R>* Vout,
+                 bool scaleV, cudaStream_t s);
+
+template <typename R>
+void launch_identity(cx<R>* out, int64_t m, cudaStream_t s);
+
+template <typename R>
+void launch_scale(cx<R>* buf, int64_t n, double f, cudaStream_t s);
+
+// sum |x|^2 into *out (double), deterministic two-stage reduction.
+template <typename R>
+void launch_sumsq(const cx<R>* buf, int64_t n, double* partial, double* out, cudaStream_t s);
+
+// MPO site (l,2,2,r) -> MPS site (l,2,r) keeping bottom index 0 (chains.py:302).
+template <typename R>
+void launch_slice_b0(const cx<R>* mpo, cx<R>* mps, int64_t l, int64_t r, cudaStream_t s);
+
+template <typename R>
+void launch_convert(const void* src, bool src_double, cx<R>* dst, int64_t n, cudaStream_t s);
+
+// Greedy marginal peak sweep over an MPS in right-canonical form.
+// dims holds (l, 2, r) per site followed by the max bond; scratch holds 3*maxbond.
+template <typename R>
+void launch_peak(const cx<R>* const* sites, const int64_t* dims, int nsites, int64_t maxbond,
+                 uint8_t* bits, double* probs, cx<R>* scratch, cudaStream_t s);
+
+// One sampling step: amp (S x 2r) from env @ site done by gemm; this picks
+// the branch per shot and writes the next env (S x r).
+template <typename R>
+void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double* uniforms,
+                        uint8_t* bits_col, int64_t bit_stride, cx<R>* env_out, cudaStream_t s);
+
+}  // namespace mb

@@ -1,0 +1,183 @@
+"""Greedy extraction of hidden permutations from a device-resident chain:
+input = P_left . reduced . P_right (reference unswap.py).
+
+The control flow (availability set, parity cycle, tie rules, acceptance) is
+host logic identical to the reference; the numerics per bond are device
+calls: the bond re-truncation is ``mb_pair_swap(recenter=1)`` with no swap,
+the left/right/both candidate extents are ONE batched ``mb_swap_extents``
+call (values-only decompositions, one CTA per candidate), and the accepted
+candidate is re-split in place with ``mb_pair_swap(recenter=0)``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .chains import MatrixProductOperator, total_elements
+from .routing import QubitPermutation
+
+_EVALUATION_SLACK = 16
+
+PARALLEL_CYCLE = (("both", 0), ("both", 1), ("left", 0), ("left", 1), ("right", 0), ("right", 1))
+
+
+@dataclass(frozen=True)
+class UnswapConfig:
+    """unswap.py:38-54 (paper App. A.1, A.2, A.4)."""
+
+    epsilon: float
+    chi_max: int
+    acceptance: str = "strict"
+    strategy: str = "sequential"
+    max_outer_iterations: int = 20
+
+    def __post_init__(self):
+        if self.acceptance not in ("strict", "relaxed"):
+            raise ValueError(f"acceptance must be strict or relaxed, got {self.acceptance!r}")
+        if self.strategy not in ("sequential", "parity-parallel"):
+            raise ValueError(
+                f"strategy must be sequential or parity-parallel, got {self.strategy!r}")
+        if self.max_outer_iterations < 1:
+            raise ValueError("max_outer_iterations must be >= 1")
+
+
+@dataclass(frozen=True)
+class UnswapResult:
+    reduced: MatrixProductOperator
+    left_perm: QubitPermutation
+    right_perm: QubitPermutation
+    accepted_swaps: int
+    elements_before: int
+    elements_after: int
+
+
+class _Work:
+    """The chain being reduced (mutated in place on the device) plus the
+    accumulated outer permutations (unswap.py:67-92)."""
+
+    def __init__(self, m: MatrixProductOperator, cfg: UnswapConfig):
+        self.m = MatrixProductOperator(m._clone_handle())
+        n = m.num_sites
+        self.n = n
+        self.left = QubitPermutation.identity(n)
+        self.right = QubitPermutation.identity(n)
+        self.accepted = 0
+        self.cfg = cfg
+        self.bonds = list(m.bond_dims())
+        self.log: list[tuple[int, str]] = []
+
+    def refresh(self):
+        # host-side metadata read (no device sync); a center move can shrink
+        # any bond it crosses, so refresh them all
+        self.bonds = [int(x) for x in self.m._bonds()[1:-1]]
+
+    def normalize(self, bond: int) -> int:
+        """Move the center to the bond and re-truncate it (unswap.py:124-134)."""
+        nat.check(nat._lib.mb_pair_swap(self.m._h, bond, 0, 0, self.cfg.epsilon,
+                                        self.cfg.chi_max, 1), "normalize bond")
+        self.refresh()
+        return self.bonds[bond]
+
+    def extents(self, bond: int, sides) -> list[int]:
+        """Values-only candidate extents, batched (unswap.py:104-112)."""
+        codes = (C.c_int * len(sides))(*(nat.SIDE[s] for s in sides))
+        out = np.zeros(len(sides), dtype=np.int64)
+        nat.check(nat._lib.mb_swap_extents(self.m._h, bond, len(sides), codes, self.cfg.epsilon,
+                                           self.cfg.chi_max, nat.i64ptr(out)), "swap extents")
+        return [int(x) for x in out]
+
+    def accept(self, bond: int, side: str) -> None:
+        """Materialize the candidate and record the swap (unswap.py:84-92, 115-121)."""
+        nat.check(nat._lib.mb_pair_swap(self.m._h, bond, int(side in ("left", "both")),
+                                        int(side in ("right", "both")), self.cfg.epsilon,
+                                        self.cfg.chi_max, 0), "apply candidate")
+        self.refresh()
+        tau = QubitPermutation.transposition(self.n, bond, bond + 1)
+        if side in ("left", "both"):
+            self.left = self.left.compose(tau)
+        if side in ("right", "both"):
+            self.right = tau.compose(self.right)
+        self.accepted += 1
+        self.log.append((bond, side))
+
+
+def _try_bond(w: _Work, bond: int, sides, seen) -> bool:
+    """unswap.py:137-167: ties prefer earlier sides (left, right, both)."""
+    baseline = w.normalize(bond)
+    todo = [s for s in sides if seen is None or (bond, s) not in seen]
+    if not todo:
+        return False
+    ext = w.extents(bond, todo)
+    best = min(range(len(todo)), key=lambda k: (ext[k], k))
+    side, extent = todo[best], ext[best]
+    if extent < baseline or (w.cfg.acceptance == "relaxed" and extent == baseline):
+        if seen is not None:
+            seen.add((bond, side))
+        w.accept(bond, side)
+        return True
+    return False
+
+
+def _result(w: _Work, before: int) -> UnswapResult:
+    return UnswapResult(reduced=w.m, left_perm=w.left, right_perm=w.right,
+                        accepted_swaps=w.accepted, elements_before=before,
+                        elements_after=total_elements(w.m))
+
+
+def unswap_sequential(m: MatrixProductOperator, cfg: UnswapConfig) -> UnswapResult:
+    """Availability-set loop over bonds ranked by extent, lowest index on
+    ties; acceptance re-enables the neighbours (unswap.py:170-211)."""
+    w = _Work(m, cfg)
+    before = total_elements(m)
+    n = w.n
+    budget = cfg.max_outer_iterations * max(1, n - 1) * 3 * _EVALUATION_SLACK
+    evals = 0
+    for _ in range(cfg.max_outer_iterations):
+        avail = set(range(n - 1))
+        seen = set() if cfg.acceptance == "relaxed" else None
+        took = 0
+        while avail:
+            evals += 1
+            if evals > budget:
+                raise RuntimeError("unswap exceeded its evaluation budget")
+            bond = max(avail, key=lambda i: (w.bonds[i], -i))
+            if _try_bond(w, bond, ("left", "right", "both"), seen):
+                took += 1
+                avail.discard(bond)
+                if bond >= 1:
+                    avail.add(bond - 1)
+                if bond + 1 <= n - 2:
+                    avail.add(bond + 1)
+            else:
+                avail.discard(bond)
+        if took == 0:
+            break
+    return _result(w, before)
+
+
+def unswap_parallel(m: MatrixProductOperator, cfg: UnswapConfig) -> UnswapResult:
+    """Parity-batched variant cycling (both, left, right) x (even, odd);
+    stops after a cycle with no bond reduction (unswap.py:214-240)."""
+    w = _Work(m, cfg)
+    before = total_elements(m)
+    n = w.n
+    for _ in range(cfg.max_outer_iterations):
+        reduced = False
+        for side, parity in PARALLEL_CYCLE:
+            for bond in range(parity, n - 1, 2):
+                was = w.bonds[bond]
+                if _try_bond(w, bond, (side,), None) and w.bonds[bond] < was:
+                    reduced = True
+        if not reduced:
+            break
+    return _result(w, before)
+
+
+def unswap(m: MatrixProductOperator, cfg: UnswapConfig) -> UnswapResult:
+    if cfg.strategy == "sequential":
+        return unswap_sequential(m, cfg)
+    return unswap_parallel(m, cfg)

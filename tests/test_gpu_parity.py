@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden fixtures.
+
+Tolerances (north_star): complex128 — integer/decision outputs (ranks,
+traces, permutations, samples, peak bits) bit-exact, amplitudes within
+1e-10; complex64 — peak bitstring bit-exact, peak probability and fidelity
+within 1e-5 relative.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import mirror_oracle as mo  # noqa: E402
+from oracle import statevector as sv  # noqa: E402
+
+import paper_2604_21908_b200 as pb  # noqa: E402
+from paper_2604_21908_b200 import _native as nat  # noqa: E402
+from paper_2604_21908_b200.chains import (  # noqa: E402
+    MatrixProductOperator,
+    absorb_gate,
+    apply_swap_boundary,
+    apply_to_zero,
+    compress,
+    extract_peak,
+    identity_mpo,
+    move_center,
+    mpo_to_dense,
+    mps_to_dense,
+    sample,
+)
+from paper_2604_21908_b200.circuit import Circuit, Gate, parse_qasm  # noqa: E402
+from paper_2604_21908_b200.driver import ContractionConfig, dense_output, peak_output, run, sample_output  # noqa: E402
+from paper_2604_21908_b200.unswap import UnswapConfig, unswap  # noqa: E402
+
+EXACT = 1e-12
+
+
+def og(g: Gate):
+    return mo.OGate(g.kind, g.qubits, g.params, g.origin != "source")
+
+
+def random_adjacent(n, count, rng):
+    kinds1 = ["h", "x", "rx", "ry", "rz", "u3"]
+    npar = {"h": 0, "x": 0, "rx": 1, "ry": 1, "rz": 1, "u3": 3}
+    gates = []
+    for _ in range(count):
+        k = kinds1[rng.integers(len(kinds1))]
+        gates.append(Gate(k, (int(rng.integers(n)),),
+                          tuple(float(x) for x in rng.uniform(-np.pi, np.pi, npar[k]))))
+        k2 = ["cx", "rzz", "swap"][rng.integers(3)]
+        a = int(rng.integers(n - 1))
+        pair = (a, a + 1) if rng.random() < 0.5 else (a + 1, a)
+        gates.append(Gate(k2, pair, (float(rng.uniform(-np.pi, np.pi)),) if k2 == "rzz" else ()))
+    return Circuit(n, tuple(gates))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    nat.load()
+    yield
+    nat.synchronize()
+
+
+# ---- truncated SVD (tensor.py:84) ------------------------------------------------
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_svd_truncate_golden(golden, golden_arrays, dtype):
+    for case in golden["svd"]:
+        a = golden_arrays[case["key"]]
+        s_ref = np.asarray(case["s"])
+        for cut in case["cuts"]:
+            if dtype == "complex64" and 0 < cut["eps"] < 1e-6:
+                continue  # below fp32 resolution
+            dec = pb.svd_truncate(a, 1, cut["eps"], cut["chi"], dtype=dtype)
+            assert dec.rank == cut["rank"], (case["key"], cut, dtype)
+            tol = 1e-12 if dtype == "complex128" else 2e-6
+            np.testing.assert_allclose(dec.s, s_ref[:dec.rank], rtol=tol, atol=tol * s_ref[0])
+            assert dec.discarded_weight == pytest.approx(cut["discarded"], rel=1e-6 if dtype == "complex64" else 1e-9, abs=1e-6 if dtype == "complex64" else 1e-14)
+            r = dec.rank
+            np.testing.assert_allclose(dec.u.conj().T @ dec.u, np.eye(r), atol=10 * tol)
+            np.testing.assert_allclose(dec.v @ dec.v.conj().T, np.eye(r), atol=10 * tol)
+            if cut["eps"] == 0.0 and cut["chi"] >= min(a.shape):
+                rec = dec.u @ np.diag(dec.s) @ dec.v
+                assert np.linalg.norm(rec - a) <= 10 * tol * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("shape", [(300, 200), (130, 400), (96, 96)])
+def test_svd_large_path(shape):
+    rng = np.random.default_rng(sum(shape))
+    a = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    # graded spectrum with an exact-rank tail
+    u, s, v = np.linalg.svd(a, full_matrices=False)
+    s = np.exp(-np.arange(len(s)) / 8.0)
+    s[len(s) // 2:] = 0.0
+    a = (u * s) @ v
+    s_ref = np.linalg.svd(a, compute_uv=False)
+    for eps in (0.0, 1e-10, 1e-3):
+        dec = pb.svd_truncate(a, 1, eps, 10**6)
+        assert dec.rank == mo.kept_rank(s_ref, eps, 10**6), eps
+        np.testing.assert_allclose(dec.s, s_ref[:dec.rank], rtol=1e-10, atol=1e-13)
+        rec = dec.u @ np.diag(dec.s) @ dec.v
+        ref = mo.tsvd(a, 1, eps, 10**6)
+        rec_ref = ref[0] @ np.diag(ref[1]) @ ref[2]
+        assert np.abs(rec - rec_ref).max() < 1e-10
+
+
+# ---- chain operations vs the oracle -------------------------------------------------
+
+@pytest.mark.parametrize("side", ["left", "right"])
+@pytest.mark.parametrize("seed", range(4))
+def test_absorb_dense_equivalence(side, seed):
+    rng = np.random.default_rng(1200 + seed)
+    c = random_adjacent(4, 6, rng)
+    m = identity_mpo(4)
+    oc = mo.identity_chain(4)
+    gates = c.gates if side == "left" else tuple(reversed(c.gates))
+    for g in gates:
+        m = absorb_gate(m, g, side, EXACT, 10**9)
+        oc = mo.absorb(oc, og(g), side, EXACT, 10**9)
+        assert m.bond_dims() == oc.bonds()
+    expected = sv.circuit_unitary(4, tuple(og(g) for g in c.gates))
+    np.testing.assert_allclose(mpo_to_dense(m), expected, atol=1e-10)
+    np.testing.assert_allclose(mpo_to_dense(m), mo.chain_dense(oc), atol=1e-10)
+
+
+def test_interleaved_left_right_and_compress():
+    rng = np.random.default_rng(90)
+    a = random_adjacent(5, 5, rng)
+    b = random_adjacent(5, 5, rng)
+    m, oc = identity_mpo(5), mo.identity_chain(5)
+    for g in reversed(a.gates):
+        m = absorb_gate(m, g, "right", 1e-10, 256)
+        oc = mo.absorb(oc, og(g), "right", 1e-10, 256)
+    for g in b.gates:
+        m = absorb_gate(m, g, "left", 1e-10, 256)
+        oc = mo.absorb(oc, og(g), "left", 1e-10, 256)
+    m2, oc2 = compress(m, 1e-10, 256), mo.compress(oc, 1e-10, 256)
+    assert m2.bond_dims() == oc2.bonds() and m2.center == 0
+    assert m2.log_norm == pytest.approx(oc2.log_norm, abs=1e-10)
+    np.testing.assert_allclose(mpo_to_dense(m2), mo.chain_dense(oc2), atol=1e-9)
+    for s in m2.sites[1:]:  # right-isometries
+        mat = s.reshape(s.shape[0], -1)
+        np.testing.assert_allclose(mat @ mat.conj().T, np.eye(s.shape[0]), atol=1e-9)
+    dense = mpo_to_dense(m2)
+    for target in (4, 1, 2, 0):
+        m2 = move_center(m2, target)
+        assert m2.center == target
+        np.testing.assert_allclose(mpo_to_dense(m2), dense, atol=1e-9)
+
+
+def test_swap_boundary_cases():
+    sw = Gate("swap", (0, 1))
+    m = absorb_gate(identity_mpo(2), sw, "left", EXACT, 64)
+    assert m.bond_dims() == (4,)
+    m2 = apply_swap_boundary(m, 0, "left", EXACT, 64)
+    assert m2.bond_dims() == (1,)
+    np.testing.assert_allclose(mpo_to_dense(m2), np.eye(4), atol=1e-12)
+    m3 = apply_swap_boundary(identity_mpo(3), 1, "both", EXACT, 64)
+    assert m3.bond_dims() == (1, 1)
+    with pytest.raises(ValueError, match="out of range"):
+        apply_swap_boundary(identity_mpo(3), 2, "left", EXACT, 64)
+
+
+def test_functional_semantics_do_not_mutate_inputs():
+    m = identity_mpo(3)
+    before = mpo_to_dense(m)
+    m2 = absorb_gate(m, Gate("cx", (0, 1)), "left", EXACT, 64)
+    m3 = compress(m2, 1e-10, 64)
+    np.testing.assert_array_equal(mpo_to_dense(m), before)
+    assert m2.center == 1 and m3.center == 0
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_apply_to_zero_sample_and_peak(seed):
+    rng = np.random.default_rng(1400 + seed)
+    c = random_adjacent(5, 8, rng)
+    m, oc = identity_mpo(5), mo.identity_chain(5)
+    for g in c.gates:
+        m = absorb_gate(m, g, "left", 1e-12, 256)
+        oc = mo.absorb(oc, og(g), "left", 1e-12, 256)
+    psi, opsi = apply_to_zero(m, 1e-12, 256), mo.to_zero_state(oc, 1e-12, 256)
+    assert psi.bond_dims() == opsi.bonds()
+    vec = mps_to_dense(psi)
+    ref = sv.simulate(5, tuple(og(g) for g in c.gates))
+    assert abs(np.vdot(ref, vec)) ** 2 >= 1 - 1e-10
+    # identical random stream -> identical draws
+    assert sample(psi, 300, seed=seed) == mo.sample_state(opsi, 300, seed)
+    bits, p = extract_peak(psi)
+    obits, op = mo.greedy_peak(opsi)
+    assert bits == obits and p == pytest.approx(op, rel=1e-10)
+
+
+# ---- unswapping (unswap.py) -------------------------------------------------------------
+
+def _perm_mpo(perm, side):
+    m = identity_mpo(len(perm))
+    swaps = mo.p_factorization(perm)
+    for i, j in (reversed(swaps) if side == "left" else swaps):
+        m = absorb_gate(m, Gate("swap", (i, j)), side, 1e-12, 4096)
+    return compress(m, 1e-12, 4096)
+
+
+def test_unswap_matches_reference(golden):
+    for case in golden["unswap"]:
+        m = _perm_mpo(tuple(case["perm"]), case["side"])
+        assert list(m.bond_dims()) == case["bonds_before"]
+        res = unswap(m, UnswapConfig(epsilon=1e-10, chi_max=4096, strategy=case["strategy"]))
+        assert res.accepted_swaps == case["accepted"], case
+        assert list(res.left_perm.mapping) == case["left"]
+        assert list(res.right_perm.mapping) == case["right"]
+        assert list(res.reduced.bond_dims()) == case["bonds_after"]
+        assert res.elements_after == case["elements_after"]
+
+
+# ---- end-to-end driver vs the reference's golden runs -------------------------------------
+
+CASES = ["mirror6", "random5_longrange", "random5_forced_unswap", "peaked6_sequential",
+         "peaked6_parity-parallel", "peaked6_relaxed", "peaked10_tau4000", "peaked12_sawtooth",
+         "config0_mirror12"]
+
+
+def _case(golden, name):
+    return next(c for c in golden["circuits"] if c["name"] == name)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_driver_matches_reference_fp64(golden, golden_arrays, name):
+    case = _case(golden, name)
+    c = parse_qasm(case["qasm"])
+    res = run(c, ContractionConfig(**case["config"]))
+    assert [[t.phase, t.unitaries_consumed, t.elements] for t in res.trace] == case["trace"]
+    assert res.final_elements == case["final_elements"]
+    assert res.chi_saturation_events == case["chi_saturation_events"]
+    assert list(res.output_permutation.mapping) == case["pi_out"]
+    assert list(res.input_permutation.mapping) == case["pi_in"]
+    assert list(res.state.bond_dims()) == case["state_bonds"]
+    assert res.state.log_norm == pytest.approx(case["state_log_norm"], abs=1e-10)
+    assert sample_output(res, 200, seed=9) == case["samples_seed9"]
+    vec = dense_output(res)
+    ref = golden_arrays[f"{name}__dense"]
+    assert abs(np.vdot(ref, vec)) ** 2 == pytest.approx(1.0, abs=1e-10)
+    np.testing.assert_allclose(vec, ref, atol=1e-9)
+    bits, p = peak_output(res)
+    assert p == pytest.approx(abs(vec[sv.index_of(bits)]) ** 2, rel=1e-10)
+    if case["planted_peak"] is not None or name.startswith("mirror"):
+        assert bits == case["oracle_peak"]
+        assert p == pytest.approx(case["oracle_peak_prob"], rel=1e-10)
+
+
+@pytest.mark.parametrize("name", ["peaked10_tau4000", "peaked12_sawtooth", "config0_mirror12"])
+def test_driver_fp32_peak_and_fidelity(golden, golden_arrays, name):
+    case = _case(golden, name)
+    c = parse_qasm(case["qasm"])
+    cfg = dict(case["config"], dtype="complex64")
+    res = run(c, ContractionConfig(**cfg))
+    bits, p = peak_output(res)
+    assert bits == case["oracle_peak"]
+    assert p == pytest.approx(case["oracle_peak_prob"], rel=1e-5)
+    vec = dense_output(res)
+    ref = golden_arrays[f"{name}__dense"]
+    assert abs(np.vdot(ref, vec)) ** 2 == pytest.approx(1.0, abs=1e-5)
+
+
+def test_config1_peaked20_matches_reference(golden):
+    case = _case(golden, "config1_peaked20")
+    c = parse_qasm(case["qasm"])
+    res = run(c, ContractionConfig(**case["config"]))
+    assert [[t.phase, t.unitaries_consumed, t.elements] for t in res.trace] == case["trace"]
+    assert list(res.output_permutation.mapping) == case["pi_out"]
+    assert sample_output(res, 200, seed=9) == case["samples_seed9"]
+    bits, p = peak_output(res)
+    assert bits == case["planted_peak"] == case["top1000_seed3"][0]
