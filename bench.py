@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark: middle-MPO contraction of the 56-qubit H2-scale obfuscated
+peaked circuit to its peak bitstring on B200 (BASELINE.json configs[3]).
+
+One step = contract the whole circuit (route, split, absorb/unswap/rewire
+loop, apply to |0..0>) and extract the peak on the device. ``value`` is
+source two-qubit gates absorbed per second over the K timed steps (the
+metric's "gates absorbed/s"); ``ms_per_step`` is the wall-clock to peak.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c56|c36|c20|c12] [--dtype complex128|complex64]
+
+Under torchrun (N>1) each rank contracts its own replica (the path has no
+data-path collective): scaling "weak", value = all
+ranks' gates / max-over-ranks time. ``--impl reference`` times the CPU
+reference arm (the oracle restatement of the reference algorithm, bit-exact
+with it) on a bounded prefix of the same contraction, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (n, depth, peak_weight, obfuscation_swaps, seed, hidden_permutation)
+    "c12": (12, 120, 0.1, 0, 7, False),
+    "c20": (20, 200, 0.1, 20, 1, True),
+    "c36": (36, 700, 0.1, 40, 1, True),
+    "c56": (56, 1917, 0.1, 60, 1, True),
+}
+METRIC = "wall-clock to peak for 56q circuit (1 B200); gates absorbed/s; TC util & HBM GB/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c56")
+    ap.add_argument("--dtype", choices=["complex128", "complex64"], default="complex128")
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0,
+                    help="CPU work per reference-arm sample (seconds, approx.)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _instance(name):
+    from paper_2604_21908_b200.peaked import generate
+
+    n, depth, w, obf, seed, hidden = CONFIGS[name]
+    return generate(n, depth, w, obf, seed, hidden_permutation=hidden)
+
+
+def _workload(name, dtype):
+    n, depth, w, obf, seed, hidden = CONFIGS[name]
+    return {"workload": f"{n}q peaked circuit, middle-MPO contraction + peak extraction",
+            "config": name, "qubits": n, "depth_budget": depth, "obfuscation_swaps": obf,
+            "seed": seed, "epsilon": 2e-3, "chi_max": 8192, "tau": 1_000_000,
+            "side_mode": "adaptive", "unswap": "parity-parallel/strict", "dtype": dtype,
+            "l2": "working set re-created every step (fresh MPO per contraction)"}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self):
+        self.rows, self._stop, self._t = [], threading.Event(), None
+
+    def start(self):
+        def loop():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", os.environ.get("LOCAL_RANK", "0")],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def cpu_reference(name, budget_s):
+    """Time the CPU reference arm (oracle restatement) on a bounded prefix of
+    the same contraction: absorb steps until ~budget_s of CPU work."""
+    from oracle import mirror_oracle as mo
+
+    inst = _instance(name)
+    n = inst.circuit.num_qubits
+    gates = tuple(mo.OGate(g.kind, g.qubits, g.params, g.origin != "source")
+                  for g in inst.circuit.gates)
+    cfg = mo.OConfig(stall_limit=3)
+    # grow the prefix until it costs about budget_s
+    steps, spent, res = 4, 0.0, None
+    while True:
+        t0 = time.perf_counter()
+        res = mo.contract(n, gates, cfg, max_steps=steps)
+        spent = time.perf_counter() - t0
+        if spent >= budget_s / 3 or steps >= 4096 or res.state is not None:
+            break
+        steps *= 2
+    consumed = sum(1 for t in res.trace if t[0] == "absorb")
+    src = res.trace[-1][1] if res.trace else 0
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return {"seconds": spent, "absorb_steps": steps, "unitaries_consumed": src,
+            "value": src / spent if spent > 0 else 0.0, "threads": threads,
+            "records": consumed}
+
+
+def gpu_prefix(name, dtype, steps):
+    """The same bounded prefix on the device (for an apples-to-apples line)."""
+    from paper_2604_21908_b200 import Contraction, ContractionConfig, _native as nat
+
+    inst = _instance(name)
+    job = Contraction(inst.circuit, ContractionConfig(dtype=dtype))
+    nat.synchronize()
+    t0 = time.perf_counter()
+    job.advance(max_steps=steps)
+    nat.synchronize()
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "unitaries_consumed": job.consumed,
+            "value": job.consumed / dt if dt > 0 else 0.0}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps_s = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(args.config, args.cpu_sample_s)
+        if i >= args.warmup:
+            steps_s.append(r)
+        sample = r
+    val = statistics.mean(r["value"] for r in steps_s)
+    ms = statistics.mean(r["seconds"] for r in steps_s) * 1e3
+    line = {"metric": METRIC, "value": val, "unit": "source 2q gates absorbed/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic (reference generator, seeded)",
+            "config": _workload(args.config, "complex128"),
+            "cpu_baseline": {"value": val, "unit": "source 2q gates absorbed/s",
+                             "cores": sample["threads"], "kind": "port",
+                             "sample": f"first {sample['absorb_steps']} absorption steps "
+                                       f"({sample['unitaries_consumed']} two-qubit gates) of the "
+                                       f"{args.config} contraction, numpy/OpenBLAS"},
+            "e2e": {"value": val, "unit": "source 2q gates absorbed/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = _args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_
+
+        dist = dist_
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    import torch
+
+    from paper_2604_21908_b200 import Contraction, ContractionConfig, _native as nat
+    from paper_2604_21908_b200.circuit import parse_qasm, serialize_qasm
+    from paper_2604_21908_b200.driver import peak_output
+
+    torch.cuda.set_device(local)
+    nat.load()
+    stream = torch.cuda.ExternalStream(nat.stream_handle())
+    inst = _instance(args.config)
+    qasm = serialize_qasm(inst.circuit)
+    cfg = ContractionConfig(dtype=args.dtype)
+    n2q = inst.circuit.two_qubit_count()
+
+    def one_step():
+        job = Contraction(inst.circuit, cfg)
+        job.advance()
+        res = job.finish()
+        return job, peak_output(res)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        nat.synchronize()
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+
+    # ---- timed region: device-resident path (circuit already loaded) ----
+    clocks = Clocks()
+    clocks.start()
+    launches0 = nat.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    peaks, jobs = [], []
+    for _ in range(args.steps):
+        job, pk = one_step()
+        peaks.append(pk)
+        jobs.append(job)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    launches = nat.launch_count() - launches0
+    t_max = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    dev_ms = float(t_max.item())
+    total_gates = n2q * args.steps * world
+    value = total_gates / (dev_ms / 1e3)
+
+    # ---- e2e: through the public API from QASM text to the host bitstring ----
+    from paper_2604_21908_b200 import peak_output as _po
+    c0 = nat.counters()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        circ = parse_qasm(qasm)
+        job = Contraction(circ, cfg)
+        job.advance()
+        bits, p = _po(job.finish())
+    e1.record(stream)
+    barrier()
+    c1 = nat.counters()
+    e2e_ms = e0.elapsed_time(e1)
+    t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t_e2e.item())
+    h2d = (c1["h2d_bytes"] - c0["h2d_bytes"]) // args.steps + len(qasm)
+    d2h = (c1["d2h_bytes"] - c0["d2h_bytes"]) // args.steps
+
+    # ---- one profiled (untimed) step: per-kernel-class device time ----
+    nat.profile_begin()
+    one_step()
+    prof = nat.profile_end()
+    hbm, bf16, src = _peaks()
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    tot_ms = sum(v["ms"] for v in prof.values())
+    d = prof[dom]
+    achieved_tf = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "source 2q gates absorbed/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128" if args.dtype == "complex128" else "c64",
+            "data": "synthetic (reference generator, seeded)",
+            "config": dict(_workload(args.config, args.dtype),
+                           parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
+            "peak": {"bits": peaks[-1][0], "probability": peaks[-1][1],
+                     "planted": inst.peak, "match": peaks[-1][0] == inst.peak},
+            "two_qubit_gates": n2q,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": {"value": total_gates / (e2e_ms / 1e3), "unit": "source 2q gates absorbed/s",
+                    "ms_per_step": e2e_ms / args.steps,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved_tf,
+                         "peak": bf16, "unit": "TFLOP/s", "frac": achieved_tf / bf16,
+                         "traffic": None, "peak_source": src,
+                         "share_of_device_time": d["ms"] / tot_ms if tot_ms else None,
+                         "note": "fp64/fp32 CUDA-core Jacobi + GEMM vs the bf16 tensor peak"},
+            "profile_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "contraction": {"trace_records": len(jobs[-1].trace), "unswap_calls": jobs[-1].unswap_calls,
+                            "accepted_swaps": jobs[-1].accepted_swaps,
+                            "max_elements": max(t.elements for t in jobs[-1].trace)},
+            "counters": nat.counters(),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            ref = cpu_reference(args.config, args.cpu_sample_s)
+            pre = gpu_prefix(args.config, args.dtype, ref["absorb_steps"])
+            line["cpu_baseline"] = {"value": ref["value"], "unit": "source 2q gates absorbed/s",
+                                    "cores": ref["threads"], "kind": "port",
+                                    "sample": f"first {ref['absorb_steps']} absorption steps "
+                                              f"({ref['unitaries_consumed']} two-qubit gates) of "
+                                              f"the same contraction, {ref['seconds']:.1f} s",
+                                    "b200_same_prefix": pre["value"]}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -61,8 +61,9 @@ long long mb_launch_count(void);
 int mb_profile_begin(void);
 int mb_profile_end(double* ms_per_class, long long* launches_per_class, double* flops_per_class);
 /* Counters: [0] small SVDs, [1] large SVDs, [2] large sweeps, [3] host syncs,
- * [4] svd non-converged, [5] max p seen. */
-int mb_counters(long long* out6);
+ * [4] svd non-converged, [5] max p seen, [6] host-to-device bytes (incl. gate
+ * matrices passed as kernel parameters), [7] device-to-host bytes. */
+int mb_counters(long long* out8);
 
 /* ---- construction / inspection --------------------------------------- */
 mb_chain* mb_identity_mpo(int n, int dtype);                          /* chains.py:83-88 */

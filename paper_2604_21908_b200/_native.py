@@ -127,9 +127,10 @@ def launch_count() -> int:
 
 
 def counters() -> dict:
-    out = (C.c_longlong * 6)()
+    out = (C.c_longlong * 8)()
     load().mb_counters(out)
-    keys = ("svd_small", "svd_large", "large_sweeps", "host_syncs", "svd_not_converged", "max_p")
+    keys = ("svd_small", "svd_large", "large_sweeps", "host_syncs", "svd_not_converged", "max_p",
+            "h2d_bytes", "d2h_bytes")
     return dict(zip(keys, (int(x) for x in out)))
 
 

@@ -66,7 +66,7 @@ struct Engine {
   static constexpr int kSlots = 4;
   Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots];
   Buf carry, env[2], amp, misc;
-  long long counters[6] = {0, 0, 0, 0, 0, 0};
+  long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [6] h2d bytes, [7] d2h bytes
   // profiling
   bool prof = false;
   std::vector<ProfRec> recs;
@@ -93,6 +93,16 @@ static void* grow(Buf& b, size_t bytes) {
     b = alloc(want);
   }
   return b->p;
+}
+
+static void h2d(void* dst, const void* src, size_t bytes) {
+  E.counters[6] += (long long)bytes;
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, E.stream), "h2d");
+}
+
+static void d2h(void* dst, const void* src, size_t bytes) {
+  E.counters[7] += (long long)bytes;
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, E.stream), "d2h");
 }
 
 static void sync() {
@@ -219,7 +229,8 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
     if (p > kSmallP) {
       double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
       ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * (double)p * (double)p * q);
-      svd_large<R>(jobs[i], reinterpret_cast<int*>(E.d_flag->p), E.h_flag, E.stream);
+      double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
+      svd_large<R>(jobs[i], reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, E.stream);
       E.counters[1]++;
       E.counters[3]++;
     }
@@ -228,14 +239,13 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
 
 // Read back kept ranks (and discarded weights) of the first `ns` slots.
 static void read_info(int ns) {
-  ck(cudaMemcpyAsync(E.h_info, E.d_info->p, sizeof(int64_t) * 3 * ns, cudaMemcpyDeviceToHost,
-                     E.stream),
-     "readback info");
-  ck(cudaMemcpyAsync(E.h_disc, E.d_disc->p, sizeof(double) * ns, cudaMemcpyDeviceToHost, E.stream),
-     "readback disc");
+  d2h(E.h_info, E.d_info->p, sizeof(int64_t) * 3 * ns);
+  d2h(E.h_disc, E.d_disc->p, sizeof(double) * ns);
   sync();
-  for (int i = 0; i < ns; ++i)
+  for (int i = 0; i < ns; ++i) {
     if (E.h_info[3 * i + 1]) E.counters[4]++;
+    E.counters[2] += E.h_info[3 * i + 2];
+  }
 }
 
 template <typename R>
@@ -246,13 +256,12 @@ static void emit(const SvdJob<R>& j, int64_t k, cx<R>* U, bool su, cx<R>* V, boo
 
 template <typename R>
 static double norm_of(const cx<R>* buf, int64_t n) {
-  void* part = grow(E.d_partial, 256 * sizeof(double));
+  void* part = grow(E.d_partial, 512 * sizeof(double));
   {
     ProfScope ps(P_OTHER, 0.0);
     launch_sumsq<R>(buf, n, (double*)part, (double*)E.d_scalar->p, E.stream);
   }
-  ck(cudaMemcpyAsync(E.h_scalar, E.d_scalar->p, sizeof(double), cudaMemcpyDeviceToHost, E.stream),
-     "readback norm");
+  d2h(E.h_scalar, E.d_scalar->p, sizeof(double));
   sync();
   return std::sqrt(E.h_scalar[0]);
 }
@@ -375,6 +384,7 @@ static void absorb_2q(mb_chain& c, int lo, const double* g4, int side, double ep
   cx<R>* th = blob<R>(c, lo, 0, l, r);
   Gate4<R> g;
   for (int i = 0; i < 16; ++i) g.g[i] = mk<R>((R)g4[2 * i], (R)g4[2 * i + 1]);
+  E.counters[6] += (long long)sizeof(g);  // travels in the kernel parameters
   {
     ProfScope ps(P_GATE, 0.0);
     launch_gate2<R>(th, g, l, r, side == MB_SIDE_LEFT, E.stream);
@@ -389,6 +399,7 @@ static void absorb_1q(mb_chain& c, int q, const double* u2, int side) {
   require(side == MB_SIDE_LEFT || side == MB_SIDE_RIGHT, "side must be left or right");
   Gate2<R> u;
   for (int i = 0; i < 4; ++i) u.g[i] = mk<R>((R)u2[2 * i], (R)u2[2 * i + 1]);
+  E.counters[6] += (long long)sizeof(u);
   Site A = c.s[q];
   Site nA = new_site<R>(A.l, 4, A.r);
   {
@@ -574,17 +585,15 @@ static void peak(const mb_chain& psi, uint8_t* bits, double* probs) {
   Buf dp = alloc(n * sizeof(void*)), dd = alloc(dims.size() * sizeof(int64_t));
   Buf db = alloc(n), dpr = alloc(n * sizeof(double));
   Buf scr = alloc((size_t)(3 * maxb) * sizeof(cx<R>));
-  ck(cudaMemcpyAsync(dp->p, ptrs.data(), n * sizeof(void*), cudaMemcpyHostToDevice, E.stream), "h2d");
-  ck(cudaMemcpyAsync(dd->p, dims.data(), dims.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
-                     E.stream),
-     "h2d");
+  h2d(dp->p, ptrs.data(), n * sizeof(void*));
+  h2d(dd->p, dims.data(), dims.size() * sizeof(int64_t));
   {
     ProfScope ps(P_OTHER, 0.0);
     launch_peak<R>((const cx<R>* const*)dp->p, (const int64_t*)dd->p, n, maxb, (uint8_t*)db->p,
                    (double*)dpr->p, (cx<R>*)scr->p, E.stream);
   }
-  ck(cudaMemcpyAsync(bits, db->p, n, cudaMemcpyDeviceToHost, E.stream), "d2h");
-  ck(cudaMemcpyAsync(probs, dpr->p, n * sizeof(double), cudaMemcpyDeviceToHost, E.stream), "d2h");
+  d2h(bits, db->p, n);
+  d2h(probs, dpr->p, n * sizeof(double));
   sync();
 }
 
@@ -600,15 +609,12 @@ static void sample(const mb_chain& psi, int64_t shots, const double* uni, uint8_
   for (int i = 0; i < n; ++i) maxb = std::max(maxb, w.s[i].r);
   Buf du = alloc((size_t)(n * shots) * sizeof(double));
   Buf db = alloc((size_t)(n * shots));
-  ck(cudaMemcpyAsync(du->p, uni, (size_t)(n * shots) * sizeof(double), cudaMemcpyHostToDevice,
-                     E.stream),
-     "h2d");
+  h2d(du->p, uni, (size_t)(n * shots) * sizeof(double));
   cx<R>* envA = (cx<R>*)grow(E.env[0], (size_t)(shots * maxb) * sizeof(cx<R>));
   cx<R>* envB = (cx<R>*)grow(E.env[1], (size_t)(shots * maxb) * sizeof(cx<R>));
   cx<R>* amp = (cx<R>*)grow(E.amp, (size_t)(shots * 2 * maxb) * sizeof(cx<R>));
   std::vector<cx<R>> ones(shots, mk<R>(1, 0));
-  ck(cudaMemcpyAsync(envA, ones.data(), shots * sizeof(cx<R>), cudaMemcpyHostToDevice, E.stream),
-     "h2d");
+  h2d(envA, ones.data(), shots * sizeof(cx<R>));
   for (int i = 0; i < n; ++i) {
     Site S = w.s[i];
     gemm<R>(false, shots, 2 * S.r, S.l, envA, S.l, P<R>(S), 2 * S.r, amp, 2 * S.r);
@@ -619,7 +625,7 @@ static void sample(const mb_chain& psi, int64_t shots, const double* uni, uint8_
     }
     std::swap(envA, envB);
   }
-  ck(cudaMemcpyAsync(bits, db->p, (size_t)(n * shots), cudaMemcpyDeviceToHost, E.stream), "d2h");
+  d2h(bits, db->p, (size_t)(n * shots));
   sync();
 }
 
@@ -629,10 +635,10 @@ template <typename R>
 static void upload(const double* host, cx<R>* dst, int64_t ne) {
   if (ne == 0) return;
   if (sizeof(R) == sizeof(double)) {
-    ck(cudaMemcpyAsync(dst, host, (size_t)ne * 16, cudaMemcpyHostToDevice, E.stream), "h2d");
+    h2d(dst, host, (size_t)ne * 16);
   } else {
     void* tmp = grow(E.misc, (size_t)ne * 16);
-    ck(cudaMemcpyAsync(tmp, host, (size_t)ne * 16, cudaMemcpyHostToDevice, E.stream), "h2d");
+    h2d(tmp, host, (size_t)ne * 16);
     launch_convert<R>(tmp, true, dst, ne, E.stream);
   }
 }
@@ -641,11 +647,11 @@ template <typename R>
 static void download(const cx<R>* src, double* host, int64_t ne) {
   if (ne == 0) return;
   if (sizeof(R) == sizeof(double)) {
-    ck(cudaMemcpyAsync(host, src, (size_t)ne * 16, cudaMemcpyDeviceToHost, E.stream), "d2h");
+    d2h(host, src, (size_t)ne * 16);
   } else {
     cx<double>* tmp = (cx<double>*)grow(E.misc, (size_t)ne * 16);
     launch_convert<double>(src, false, tmp, ne, E.stream);
-    ck(cudaMemcpyAsync(host, tmp, (size_t)ne * 16, cudaMemcpyDeviceToHost, E.stream), "d2h");
+    d2h(host, tmp, (size_t)ne * 16);
   }
 }
 
@@ -695,7 +701,7 @@ static void svd_host(const double* a, int64_t m, int64_t n, double eps, int64_t 
   Buf dU = alloc((size_t)(m * k) * sizeof(cx<R>)), dV = alloc((size_t)(k * n) * sizeof(cx<R>));
   emit<R>(j, k, (cx<R>*)dU->p, false, (cx<R>*)dV->p, false);
   std::vector<R> sg(k);
-  ck(cudaMemcpyAsync(sg.data(), j.sig, k * sizeof(R), cudaMemcpyDeviceToHost, E.stream), "d2h");
+  d2h(sg.data(), j.sig, k * sizeof(R));
   sync();
   download<R>((cx<R>*)dU->p, u, m * k);
   sync();
@@ -819,8 +825,8 @@ int mb_profile_end(double* ms, long long* launches, double* flops) {
   });
 }
 
-int mb_counters(long long* out6) {
-  for (int i = 0; i < 6; ++i) out6[i] = E.counters[i];
+int mb_counters(long long* out8) {
+  for (int i = 0; i < 8; ++i) out8[i] = E.counters[i];
   return 0;
 }
 

@@ -10,6 +10,8 @@
 //  * k_peak          : single-CTA sequential MPS marginal sweep.
 #include "mb_kernels.cuh"
 
+#include <cooperative_groups.h>
+
 #include <atomic>
 #include <cstdio>
 #include <vector>
@@ -17,6 +19,7 @@
 namespace mb {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__device__ __forceinline__ int64_t cdiv_d(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
@@ -216,11 +219,23 @@ void launch_gate1(const cx<R>* src, cx<R>* dst, const Gate2<R>& u, int64_t l, in
 // ---------------------------------------------------------------------------
 
 constexpr int TQ = 32;  // rows of X staged per chunk
+constexpr int kSumBlocks = 256;
+
+template <typename R>
+__global__ void k_sumsq_partial(const cx<R>* __restrict__ buf, int64_t n, double* partial);
+__global__ void k_sumsq_final(const double* partial, int nb, double* out);
 
 template <typename R>
 __device__ __forceinline__ double rel_tol(int64_t q) {
   double s = sqrt((double)(q > 1 ? q : 1));
   return (s > 8.0 ? s : 8.0) * 4.0 * Eps<R>::u;
+}
+
+// absolute floor factor: the floor is abs_floor * ||A||_F^2
+template <typename R>
+__device__ __forceinline__ double abs_floor(int64_t q) {
+  (void)q;
+  return 4.0 * Eps<R>::u;
 }
 
 // Tournament (circle method) pairing for NP even: round rnd, pair i.
@@ -245,7 +260,9 @@ struct PairSmem {
 
 // Gram of the selected columns: h[a][b] = x_a^H x_b over all q rows.
 template <typename R, int W2>
-__device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64_t q) {
+__device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64_t q,
+                          int64_t r0 = 0, int64_t r1 = -1) {
+  if (r1 < 0) r1 = q;
   constexpr int TM = W2 / 16;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   cx<R> acc[TM][TM];
@@ -253,11 +270,11 @@ __device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TM; ++j) acc[i][j] = mk<R>(0, 0);
-  for (int64_t i0 = 0; i0 < q; i0 += TQ) {
+  for (int64_t i0 = r0; i0 < r1; i0 += TQ) {
     for (int e = tid; e < W2 * TQ; e += blockDim.x) {
       int c = e / TQ, t = e % TQ;
       int gc = S.col[c];
-      S.xs[c][t] = (gc >= 0 && i0 + t < q) ? X[(int64_t)gc * q + i0 + t] : mk<R>(0, 0);
+      S.xs[c][t] = (gc >= 0 && i0 + t < r1) ? X[(int64_t)gc * q + i0 + t] : mk<R>(0, 0);
     }
     __syncthreads();
 #pragma unroll 4
@@ -281,34 +298,47 @@ __device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64
   __syncthreads();
 }
 
-// Is the Gram off-diagonal above tolerance (relative to the diagonal)?
+// Is the Gram off-diagonal above tolerance? A pair (a, b) still needs a
+// rotation iff |h_ab| exceeds BOTH the relative bound tol*sqrt(h_aa h_bb) and
+// the absolute floor (u-level of ||A||_F^2). The floor gives the backward-stable
+// accuracy class of LAPACK's gesdd (absolute error ~u*sigma_max in every
+// singular value); without it numerically rank-deficient blocks never
+// converge because their noise columns cannot be made relatively orthogonal.
 template <typename R, int W2>
-__device__ bool pair_offdiag(PairSmem<R, W2>& S, double tol) {
+__device__ bool pair_offdiag(PairSmem<R, W2>& S, double tol, double floor_abs) {
   if (threadIdx.x == 0) S.flag = 0;
   __syncthreads();
-  double t2 = tol * tol;
+  const double t2 = tol * tol, f2 = floor_abs * floor_abs;
   for (int e = threadIdx.x; e < W2 * W2; e += blockDim.x) {
     int a = e / W2, b = e % W2;
     if (a >= b) continue;
     double haa = S.h[a][a].x, hbb = S.h[b][b].x;
     double g2 = (double)cabs2(S.h[a][b]);
-    if (haa > 0 && hbb > 0 && g2 > t2 * haa * hbb) S.flag = 1;
+    if (haa > 0 && hbb > 0 && g2 > t2 * haa * hbb && g2 > f2) S.flag = 1;
   }
   __syncthreads();
   return S.flag != 0;
 }
 
+// trace of the staged Gram (= ||selected columns||_F^2), read by all threads
+template <typename R, int W2>
+__device__ double pair_trace(PairSmem<R, W2>& S) {
+  double t = 0;
+  for (int c = 0; c < W2; ++c) t += (double)S.h[c][c].x;
+  return t;
+}
+
 // Two-sided cyclic Jacobi on the Hermitian h; accumulates the rotation in w.
 template <typename R, int W2>
-__device__ void pair_evd(PairSmem<R, W2>& S, double tol) {
+__device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int max_sweeps) {
   const int tid = threadIdx.x;
   for (int e = tid; e < W2 * W2; e += blockDim.x) {
     int a = e / W2, b = e % W2;
     S.w[a][b] = mk<R>(a == b ? 1 : 0, 0);
   }
   __syncthreads();
-  const double t2 = tol * tol;
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  const double t2 = tol * tol, f2 = floor_abs * floor_abs;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) S.flag = 0;
     __syncthreads();
     for (int rnd = 0; rnd < W2 - 1; ++rnd) {
@@ -321,7 +351,7 @@ __device__ void pair_evd(PairSmem<R, W2>& S, double tol) {
         double a = S.h[j][j].x, b = S.h[k][k].x;
         cx<R> g = S.h[j][k];
         double ga2 = (double)cabs2(g);
-        if (a > 0 && b > 0 && ga2 > t2 * a * b) {
+        if (a > 0 && b > 0 && ga2 > t2 * a * b && ga2 > f2) {
           double ga = sqrt(ga2);
           double zeta = (b - a) / (2.0 * ga);
           double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -374,19 +404,21 @@ __device__ void pair_evd(PairSmem<R, W2>& S, double tol) {
 
 // Y[:, cols] <- Y[:, cols] W for a column-major matrix with column length len.
 template <typename R, int W2>
-__device__ void pair_apply(PairSmem<R, W2>& S, cx<R>* __restrict__ Y, int64_t len) {
+__device__ void pair_apply(PairSmem<R, W2>& S, cx<R>* __restrict__ Y, int64_t len,
+                           int64_t r0 = 0, int64_t r1 = -1) {
   const int tid = threadIdx.x;
-  for (int64_t i0 = 0; i0 < len; i0 += TQ) {
+  if (r1 < 0) r1 = len;
+  for (int64_t i0 = r0; i0 < r1; i0 += TQ) {
     for (int e = tid; e < W2 * TQ; e += blockDim.x) {
       int c = e / TQ, t = e % TQ;
       int gc = S.col[c];
-      S.xs[c][t] = (gc >= 0 && i0 + t < len) ? Y[(int64_t)gc * len + i0 + t] : mk<R>(0, 0);
+      S.xs[c][t] = (gc >= 0 && i0 + t < r1) ? Y[(int64_t)gc * len + i0 + t] : mk<R>(0, 0);
     }
     __syncthreads();
     for (int e = tid; e < W2 * TQ; e += blockDim.x) {
       int c = e / TQ, t = e % TQ;
       int gc = S.col[c];
-      if (gc < 0 || i0 + t >= len) continue;
+      if (gc < 0 || i0 + t >= r1) continue;
       cx<R> acc = mk<R>(0, 0);
 #pragma unroll 8
       for (int c2 = 0; c2 < W2; ++c2) cfma(acc, S.xs[c2][t], S.w[c2][c]);
@@ -414,8 +446,16 @@ __device__ void rank_rule(const R* sig, int p, double eps, int64_t chi, int64_t*
     else break;
     tail += (double)sig[k - 1] * (double)sig[k - 1];
   }
+  // tensor.py:132-134 keeps values within 1e-12 of the boundary together; in
+  // complex64 that gap is below resolution, so ties there are values within a
+  // few fp32 ulps of the largest singular value.
+  double tie = 1e-12;
+  if (sizeof(R) == sizeof(float)) {
+    double t32 = 64.0 * Eps<float>::u * (double)sig[0];
+    tie = t32 > tie ? t32 : tie;
+  }
   double edge = sig[r - 1];
-  while (r < p && (double)sig[r] >= edge - 1e-12) ++r;
+  while (r < p && (double)sig[r] >= edge - tie) ++r;
   int64_t rk = r < chi ? r : chi;
   double disc = 0;
   for (int k = (int)rk; k < p; ++k) disc += (double)sig[k] * (double)sig[k];
@@ -463,8 +503,9 @@ __global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
   int it = 0, converged = 0;
   for (; it < 16; ++it) {
     pair_gram<R, W2>(S, J.X, q);
-    if (!pair_offdiag<R, W2>(S, tol)) { converged = 1; break; }
-    pair_evd<R, W2>(S, tol);
+    const double fl = abs_floor<R>(q) * pair_trace<R, W2>(S);
+    if (!pair_offdiag<R, W2>(S, tol, fl)) { converged = 1; break; }
+    pair_evd<R, W2>(S, tol, fl, 30);
     pair_apply<R, W2>(S, J.X, q);
     if (J.V) pair_apply<R, W2>(S, J.V, p);
   }
@@ -551,7 +592,9 @@ __global__ void k_init_large(const cx<R>* __restrict__ A, cx<R>* __restrict__ X,
 template <typename R, int W2>
 __global__ void __launch_bounds__(256) k_jacobi_pair(cx<R>* __restrict__ X, cx<R>* __restrict__ V,
                                                      int64_t p, int64_t q, int nb, int NB, int rnd,
-                                                     int* __restrict__ flag) {
+                                                     int* __restrict__ flag,
+                                                     const double* __restrict__ fro2,
+                                                     int inner_sweeps) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
   constexpr int w = W2 / 2;
@@ -564,12 +607,79 @@ __global__ void __launch_bounds__(256) k_jacobi_pair(cx<R>* __restrict__ X, cx<R
   }
   __syncthreads();
   const double tol = rel_tol<R>(q);
+  const double fl = abs_floor<R>(q) * (*fro2);
   pair_gram<R, W2>(S, X, q);
-  if (!pair_offdiag<R, W2>(S, tol)) return;
-  pair_evd<R, W2>(S, tol);
+  if (!pair_offdiag<R, W2>(S, tol, fl)) return;
+  pair_evd<R, W2>(S, tol, fl, inner_sweeps);
   pair_apply<R, W2>(S, X, q);
   if (V) pair_apply<R, W2>(S, V, p);
   if (threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// Cluster variant: the CL CTAs of a cluster share one block pair. Each CTA
+// forms the partial Gram of its slice of rows; the partials are summed
+// through distributed shared memory into rank 0, which runs the inner EVD;
+// the rotation is read back by every CTA over DSMEM and applied to its own
+// rows of X and V. One launch per tournament round, no global round trips.
+template <typename R, int W2, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
+    k_jacobi_pair_cl(cx<R>* __restrict__ X, cx<R>* __restrict__ V, int64_t p, int64_t q, int nb,
+                     int NB, int rnd, int* __restrict__ flag, const double* __restrict__ fro2,
+                     int inner_sweeps) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  constexpr int w = W2 / 2;
+  int a, b;
+  tournament(NB, rnd, blockIdx.x / CL, a, b);
+  for (int c = threadIdx.x; c < W2; c += blockDim.x) {
+    int blk = c < w ? a : b;
+    int64_t gc = (int64_t)blk * w + (c % w);
+    S.col[c] = (blk < nb && gc < p) ? (int)gc : -1;
+  }
+  __syncthreads();
+  const int64_t qs = cdiv_d(q, CL), q0 = rank * qs, q1 = q0 + qs < q ? q0 + qs : q;
+  pair_gram<R, W2>(S, X, q, q0, q1);
+  cluster.sync();
+  // sum the partial Grams: CTA r owns entries e = r (mod CL) and writes the
+  // total into rank 0's h
+  PairSmem<R, W2>* S0 = cluster.map_shared_rank(&S, 0);
+  for (int e = threadIdx.x * CL + rank; e < W2 * W2; e += blockDim.x * CL) {
+    int i = e / W2, j = e % W2;
+    cx<R> acc = mk<R>(0, 0);
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      PairSmem<R, W2>* Sr = cluster.map_shared_rank(&S, r);
+      acc = cadd(acc, Sr->h[i][j]);
+    }
+    S0->h[i][j] = acc;
+  }
+  cluster.sync();
+  if (rank == 0) {
+    const double tol = rel_tol<R>(q);
+    const double fl = abs_floor<R>(q) * (*fro2);
+    bool rot = pair_offdiag<R, W2>(S, tol, fl);
+    if (rot) pair_evd<R, W2>(S, tol, fl, inner_sweeps);
+    if (threadIdx.x == 0) {
+      S.flag = rot ? 1 : 0;
+      if (rot) atomicOr(flag, 1);
+    }
+  }
+  cluster.sync();
+  const int rot = S0->flag;
+  if (rot) {
+    if (rank != 0)
+      for (int e = threadIdx.x; e < W2 * W2; e += blockDim.x) S.w[e / W2][e % W2] = S0->w[e / W2][e % W2];
+  }
+  cluster.sync();  // rank 0's shared memory stays live until every CTA has its copy
+  if (!rot) return;
+  pair_apply<R, W2>(S, X, q, q0, q1);
+  if (V) {
+    const int64_t ps = cdiv_d(p, CL), p0 = rank * ps, p1 = p0 + ps < p ? p0 + ps : p;
+    if (p0 < p1) pair_apply<R, W2>(S, V, p, p0, p1);
+  }
 }
 
 template <typename R>
@@ -615,8 +725,9 @@ __global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
 }
 
 template <typename R>
-void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, cudaStream_t s) {
-  constexpr int W2 = 64;
+void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
+               cudaStream_t s) {
+  constexpr int W2 = 32;
   constexpr int w = W2 / 2;
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   if (J.A) {
@@ -624,19 +735,33 @@ void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, cudaStream_t s
     k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n);
     MB_LAUNCH_CHECK();
   }
+  // ||A||_F^2 (rotation-invariant) for the absolute convergence floor
+  double* fro2 = scratch_dev + kSumBlocks;
+  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, scratch_dev);
+  MB_LAUNCH_CHECK();
+  k_sumsq_final<<<1, 256, 0, s>>>(scratch_dev, kSumBlocks, fro2);
+  MB_LAUNCH_CHECK();
   const int nb = (int)cdiv(p, w);
   const int NB = nb + (nb & 1);
   size_t sm = sizeof(PairSmem<R, W2>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_pair<R, W2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
+  // rows per CTA: keep >= 64 rows per CTA, prefer 8-wide clusters when pairs are few
+  const bool wide = (NB / 2) * 4 < 148 && q >= 8 * 64;
   int sweeps = 0, conv = 0;
   for (; sweeps < 40; ++sweeps) {
     cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
     for (int rnd = 0; rnd < NB - 1; ++rnd) {
-      k_jacobi_pair<R, W2><<<NB / 2, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd, flag_dev);
+      if (wide)
+        k_jacobi_pair_cl<R, W2, 8><<<(NB / 2) * 8, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd,
+                                                                 flag_dev, fro2, 1);
+      else
+        k_jacobi_pair_cl<R, W2, 4><<<(NB / 2) * 4, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd,
+                                                                 flag_dev, fro2, 1);
       MB_LAUNCH_CHECK();
     }
     cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
@@ -648,7 +773,7 @@ void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, cudaStream_t s
   MB_LAUNCH_CHECK();
   k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
   MB_LAUNCH_CHECK();
-  k_rank<R><<<1, 32, 0, s>>>(J, p, conv, sweeps);
+  k_rank<R><<<1, 32, 0, s>>>(J, p, conv, sweeps + 1);
   MB_LAUNCH_CHECK();
 }
 
@@ -737,8 +862,6 @@ void launch_scale(cx<R>* buf, int64_t n, double f, cudaStream_t s) {
   k_scale<R><<<blocks, 256, 0, s>>>(buf, n, f);
   MB_LAUNCH_CHECK();
 }
-
-constexpr int kSumBlocks = 256;
 
 template <typename R>
 __global__ void k_sumsq_partial(const cx<R>* __restrict__ buf, int64_t n, double* partial) {
@@ -924,7 +1047,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_gate1<R>(const cx<R>*, cx<R>*, const Gate2<R>&, int64_t, int64_t, bool,   \
                                 cudaStream_t);                                                  \
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
-  template void svd_large<R>(const SvdJob<R>&, int*, int*, cudaStream_t);                       \
+  template void svd_large<R>(const SvdJob<R>&, int*, int*, double*, cudaStream_t);              \
   template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
                                cudaStream_t);                                                   \
   template void launch_identity<R>(cx<R>*, int64_t, cudaStream_t);                              \

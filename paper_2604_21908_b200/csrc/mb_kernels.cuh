@@ -59,9 +59,11 @@ void launch_gate1(const cx<R>* src, cx<R>* dst, const Gate2<R>& u, int64_t l, in
 template <typename R>
 void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t s);
 
-// Large SVD (p > kSmallP): host-driven block Jacobi sweeps.
+// Large SVD (p > kSmallP): host-driven block Jacobi sweeps. scratch_dev holds
+// >= 257 doubles (norm reduction).
 template <typename R>
-void svd_large(const SvdJob<R>& job, int* flag_dev, int* flag_host, cudaStream_t s);
+void svd_large(const SvdJob<R>& job, int* flag_dev, int* flag_host, double* scratch_dev,
+               cudaStream_t s);
 
 // Write truncated factors: Uout (m x k) = U[:, :k] (* sigma if scaleU),
 // Vout (k x n) = (sigma if scaleV *) Vh[:k, :]. Either pointer may be null.
