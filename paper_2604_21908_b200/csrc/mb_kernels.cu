@@ -231,11 +231,11 @@ __device__ __forceinline__ double rel_tol(int64_t q) {
   return (s > 8.0 ? s : 8.0) * 4.0 * Eps<R>::u;
 }
 
-// absolute floor factor: the floor is abs_floor * ||A||_F^2
+// backward-stability floor factor: the floor is abs_floor * ||A||_F
 template <typename R>
 __device__ __forceinline__ double abs_floor(int64_t q) {
   (void)q;
-  return 4.0 * Eps<R>::u;
+  return 16.0 * Eps<R>::u;
 }
 
 // Tournament (circle method) pairing for NP even: round rnd, pair i.
@@ -300,10 +300,12 @@ __device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64
 
 // Is the Gram off-diagonal above tolerance? A pair (a, b) still needs a
 // rotation iff |h_ab| exceeds BOTH the relative bound tol*sqrt(h_aa h_bb) and
-// the absolute floor (u-level of ||A||_F^2). The floor gives the backward-stable
-// accuracy class of LAPACK's gesdd (absolute error ~u*sigma_max in every
-// singular value); without it numerically rank-deficient blocks never
-// converge because their noise columns cannot be made relatively orthogonal.
+// the backward-stability floor fl*sqrt(max(h_aa, h_bb)), fl = c*u*||A||_F:
+// a column that is numerically zero (norm ~u*||A||) counts as orthogonal to a
+// large column once its component along it is below ~u*||A||, which is
+// LAPACK gesdd's accuracy class (absolute error ~u*sigma_max per singular
+// value). Without the floor such noise columns never become *relatively*
+// orthogonal and the sweeps do not terminate.
 template <typename R, int W2>
 __device__ bool pair_offdiag(PairSmem<R, W2>& S, double tol, double floor_abs) {
   if (threadIdx.x == 0) S.flag = 0;
@@ -314,7 +316,7 @@ __device__ bool pair_offdiag(PairSmem<R, W2>& S, double tol, double floor_abs) {
     if (a >= b) continue;
     double haa = S.h[a][a].x, hbb = S.h[b][b].x;
     double g2 = (double)cabs2(S.h[a][b]);
-    if (haa > 0 && hbb > 0 && g2 > t2 * haa * hbb && g2 > f2) S.flag = 1;
+    if (haa > 0 && hbb > 0 && g2 > t2 * haa * hbb && g2 > f2 * (haa > hbb ? haa : hbb)) S.flag = 1;
   }
   __syncthreads();
   return S.flag != 0;
@@ -351,7 +353,7 @@ __device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int m
         double a = S.h[j][j].x, b = S.h[k][k].x;
         cx<R> g = S.h[j][k];
         double ga2 = (double)cabs2(g);
-        if (a > 0 && b > 0 && ga2 > t2 * a * b && ga2 > f2) {
+        if (a > 0 && b > 0 && ga2 > t2 * a * b && ga2 > f2 * (a > b ? a : b)) {
           double ga = sqrt(ga2);
           double zeta = (b - a) / (2.0 * ga);
           double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
   int it = 0, converged = 0;
   for (; it < 16; ++it) {
     pair_gram<R, W2>(S, J.X, q);
-    const double fl = abs_floor<R>(q) * pair_trace<R, W2>(S);
+    const double fl = abs_floor<R>(q) * sqrt(pair_trace<R, W2>(S));
     if (!pair_offdiag<R, W2>(S, tol, fl)) { converged = 1; break; }
     pair_evd<R, W2>(S, tol, fl, 30);
     pair_apply<R, W2>(S, J.X, q);
@@ -607,7 +609,7 @@ __global__ void __launch_bounds__(256) k_jacobi_pair(cx<R>* __restrict__ X, cx<R
   }
   __syncthreads();
   const double tol = rel_tol<R>(q);
-  const double fl = abs_floor<R>(q) * (*fro2);
+  const double fl = abs_floor<R>(q) * sqrt(*fro2);
   pair_gram<R, W2>(S, X, q);
   if (!pair_offdiag<R, W2>(S, tol, fl)) return;
   pair_evd<R, W2>(S, tol, fl, inner_sweeps);
@@ -659,7 +661,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
   cluster.sync();
   if (rank == 0) {
     const double tol = rel_tol<R>(q);
-    const double fl = abs_floor<R>(q) * (*fro2);
+    const double fl = abs_floor<R>(q) * sqrt(*fro2);
     bool rot = pair_offdiag<R, W2>(S, tol, fl);
     if (rot) pair_evd<R, W2>(S, tol, fl, inner_sweeps);
     if (threadIdx.x == 0) {
