@@ -14,6 +14,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 namespace mb {
@@ -666,7 +667,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
     if (rot) pair_evd<R, W2>(S, tol, fl, inner_sweeps);
     if (threadIdx.x == 0) {
       S.flag = rot ? 1 : 0;
-      if (rot) atomicOr(flag, 1);
+      if (rot) atomicAdd(flag, 1);  // rotated pairs this sweep
     }
   }
   cluster.sync();
@@ -726,18 +727,41 @@ __global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
   }
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <typename R, int W2, int CL>
+static void launch_round(const SvdJob<R>& J, int64_t p, int64_t q, int nb, int NB, int rnd,
+                         int* flag_dev, const double* fro2, int inner, cudaStream_t s) {
+  size_t sm = sizeof(PairSmem<R, W2>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    attr = true;
+  }
+  k_jacobi_pair_cl<R, W2, CL><<<(NB / 2) * CL, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd, flag_dev,
+                                                               fro2, inner);
+  MB_LAUNCH_CHECK();
+}
+
 template <typename R>
 void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
                cudaStream_t s) {
-  constexpr int W2 = 32;
-  constexpr int w = W2 / 2;
+  // block width and inner EVD sweeps per pair step (tunable for experiments)
+  static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : 32;
+  static const int inner = env_int("MB_JACOBI_INNER", 1);
+  static const int debug = env_int("MB_JACOBI_DEBUG", 0);
+  const int w = W2 / 2;
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   if (J.A) {
     int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
     k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n);
     MB_LAUNCH_CHECK();
   }
-  // ||A||_F^2 (rotation-invariant) for the absolute convergence floor
+  // ||A||_F^2 (rotation-invariant) for the backward-stability floor
   double* fro2 = scratch_dev + kSumBlocks;
   k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, scratch_dev);
   MB_LAUNCH_CHECK();
@@ -745,29 +769,24 @@ void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratc
   MB_LAUNCH_CHECK();
   const int nb = (int)cdiv(p, w);
   const int NB = nb + (nb & 1);
-  size_t sm = sizeof(PairSmem<R, W2>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
-  // rows per CTA: keep >= 64 rows per CTA, prefer 8-wide clusters when pairs are few
+  // 8-CTA clusters when the pairs alone cannot fill the chip
   const bool wide = (NB / 2) * 4 < 148 && q >= 8 * 64;
   int sweeps = 0, conv = 0;
-  for (; sweeps < 40; ++sweeps) {
+  for (; sweeps < 60; ++sweeps) {
     cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
     for (int rnd = 0; rnd < NB - 1; ++rnd) {
-      if (wide)
-        k_jacobi_pair_cl<R, W2, 8><<<(NB / 2) * 8, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd,
-                                                                 flag_dev, fro2, 1);
-      else
-        k_jacobi_pair_cl<R, W2, 4><<<(NB / 2) * 4, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd,
-                                                                 flag_dev, fro2, 1);
-      MB_LAUNCH_CHECK();
+      if (W2 == 64) {
+        if (wide) launch_round<R, 64, 8>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
+        else launch_round<R, 64, 4>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
+      } else {
+        if (wide) launch_round<R, 32, 8>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
+        else launch_round<R, 32, 4>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
+      }
     }
     cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+    if (debug) fprintf(stderr, "[svd_large p=%lld q=%lld] sweep %d rotated pairs %d of %d\n",
+                       (long long)p, (long long)q, sweeps, *flag_host, (NB / 2) * (NB - 1));
     if (*flag_host == 0) { conv = 1; break; }
   }
   // column norms into sig[p:2p] (the engine sizes sig for 2p), then sort into sig[0:p]
