@@ -126,31 +126,47 @@ def _peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def cpu_reference(name, budget_s):
-    """Time the CPU reference arm (oracle restatement) on a bounded prefix of
-    the same contraction: absorb steps until ~budget_s of CPU work."""
+def _oracle_circuit(name):
     from oracle import mirror_oracle as mo
 
     inst = _instance(name)
-    n = inst.circuit.num_qubits
     gates = tuple(mo.OGate(g.kind, g.qubits, g.params, g.origin != "source")
                   for g in inst.circuit.gates)
-    cfg = mo.OConfig(stall_limit=3)
-    # grow the prefix until it costs about budget_s
-    steps, spent, res = 4, 0.0, None
+    return inst.circuit.num_qubits, gates
+
+
+def cpu_prefix_steps(name, budget_s):
+    """Number of absorption steps of the CPU reference arm that costs about
+    budget_s seconds (doubling search; untimed). None = the whole job fits."""
+    from oracle import mirror_oracle as mo
+
+    n, gates = _oracle_circuit(name)
+    steps = 4
     while True:
         t0 = time.perf_counter()
-        res = mo.contract(n, gates, cfg, max_steps=steps)
+        res = mo.contract(n, gates, mo.OConfig(), max_steps=steps)
         spent = time.perf_counter() - t0
-        if spent >= budget_s / 3 or steps >= 4096 or res.state is not None:
-            break
+        if res.state is not None:
+            return None
+        if spent >= budget_s / 2.5 or steps >= 1 << 14:
+            return steps
         steps *= 2
-    consumed = sum(1 for t in res.trace if t[0] == "absorb")
-    src = res.trace[-1][1] if res.trace else 0
+
+
+def cpu_reference(name, steps):
+    """Time the CPU reference arm (the oracle: the reference's algorithm and
+    numpy/OpenBLAS calls, bit-exact with it) on the first `steps` absorption
+    steps of the same contraction (or the whole job if steps is None)."""
+    from oracle import mirror_oracle as mo
+
+    n, gates = _oracle_circuit(name)
+    t0 = time.perf_counter()
+    res = mo.contract(n, gates, mo.OConfig(), max_steps=steps)
+    spent = time.perf_counter() - t0
     threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
-    return {"seconds": spent, "absorb_steps": steps, "unitaries_consumed": src,
-            "value": src / spent if spent > 0 else 0.0, "threads": threads,
-            "records": consumed}
+    return {"seconds": spent, "absorb_steps": steps, "source_gates": res.consumed_source,
+            "value": res.consumed_source / spent if spent > 0 else 0.0, "threads": threads,
+            "complete": res.state is not None}
 
 
 def gpu_prefix(name, dtype, steps):
@@ -164,32 +180,36 @@ def gpu_prefix(name, dtype, steps):
     job.advance(max_steps=steps)
     nat.synchronize()
     dt = time.perf_counter() - t0
-    return {"seconds": dt, "unitaries_consumed": job.consumed,
-            "value": job.consumed / dt if dt > 0 else 0.0}
+    return {"seconds": dt, "source_gates": job.consumed_source,
+            "value": job.consumed_source / dt if dt > 0 else 0.0}
+
+
+def _sample_text(name, r):
+    what = (f"first {r['absorb_steps']} absorption steps" if r["absorb_steps"] is not None
+            else "the complete contraction")
+    return (f"{what} ({r['source_gates']} source two-qubit gates) of the {name} contraction, "
+            f"{r['seconds']:.1f} s, numpy/OpenBLAS {r['threads']} threads")
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    steps_s = []
-    sample = None
+    steps = cpu_prefix_steps(args.config, args.cpu_sample_s)
+    timed = []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference(args.config, args.cpu_sample_s)
+        r = cpu_reference(args.config, steps)
         if i >= args.warmup:
-            steps_s.append(r)
-        sample = r
-    val = statistics.mean(r["value"] for r in steps_s)
-    ms = statistics.mean(r["seconds"] for r in steps_s) * 1e3
+            timed.append(r)
+    val = statistics.mean(r["value"] for r in timed)
+    ms = statistics.mean(r["seconds"] for r in timed) * 1e3
     line = {"metric": METRIC, "value": val, "unit": "source 2q gates absorbed/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic (reference generator, seeded)",
             "config": _workload(args.config, "complex128"),
             "cpu_baseline": {"value": val, "unit": "source 2q gates absorbed/s",
-                             "cores": sample["threads"], "kind": "port",
-                             "sample": f"first {sample['absorb_steps']} absorption steps "
-                                       f"({sample['unitaries_consumed']} two-qubit gates) of the "
-                                       f"{args.config} contraction, numpy/OpenBLAS"},
+                             "cores": timed[-1]["threads"], "kind": "port",
+                             "sample": _sample_text(args.config, timed[-1])},
             "e2e": {"value": val, "unit": "source 2q gates absorbed/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -331,14 +351,15 @@ def main():
             "counters": nat.counters(),
         }
         if not args.no_cpu_baseline and world == 1:
-            ref = cpu_reference(args.config, args.cpu_sample_s)
-            pre = gpu_prefix(args.config, args.dtype, ref["absorb_steps"])
+            steps = cpu_prefix_steps(args.config, args.cpu_sample_s)
+            ref = cpu_reference(args.config, steps)
+            pre = gpu_prefix(args.config, args.dtype, steps)
             line["cpu_baseline"] = {"value": ref["value"], "unit": "source 2q gates absorbed/s",
                                     "cores": ref["threads"], "kind": "port",
-                                    "sample": f"first {ref['absorb_steps']} absorption steps "
-                                              f"({ref['unitaries_consumed']} two-qubit gates) of "
-                                              f"the same contraction, {ref['seconds']:.1f} s",
-                                    "b200_same_prefix": pre["value"]}
+                                    "sample": _sample_text(args.config, ref),
+                                    "b200_same_sample": pre["value"],
+                                    "b200_same_sample_speedup": pre["value"] / ref["value"]
+                                    if ref["value"] else None}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

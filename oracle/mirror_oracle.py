@@ -726,6 +726,7 @@ class OResult:
     final_elements: int
     chi_saturations: int
     unswap_logs: list    # per unswap call: list of accepted (bond, side)
+    consumed_source: int = 0
 
 
 def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None):
@@ -771,7 +772,7 @@ def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None):
                 sat += 1
             trace.append(("absorb", consumed, c.elements()))
             if max_steps is not None and step >= max_steps:
-                return OResult(None, pi_out, pi_in, trace, c.elements(), sat, logs)
+                return OResult(None, pi_out, pi_in, trace, c.elements(), sat, logs, consumed_src)
         if not (left.gates or right.gates):
             break
         before = c.elements()
@@ -793,7 +794,7 @@ def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None):
     if consumed_src != src_total:
         raise AssertionError("layer accounting bug")
     psi = to_zero_state(c, cfg.epsilon, cfg.chi_max)
-    return OResult(psi, pi_out, pi_in, trace, c.elements(), sat, logs)
+    return OResult(psi, pi_out, pi_in, trace, c.elements(), sat, logs, consumed_src)
 
 
 def sample_result(res: OResult, shots, seed):
