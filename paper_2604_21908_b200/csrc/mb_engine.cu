@@ -64,7 +64,7 @@ struct Engine {
   Buf d_info, d_disc, d_flag, d_partial, d_scalar;
   // grow-only scratch
   static constexpr int kSlots = 4;
-  Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots];
+  Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots], W[kSlots];
   Buf carry, env[2], amp, misc;
   long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [6] h2d bytes, [7] d2h bytes
   // profiling
@@ -197,6 +197,8 @@ static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double
   j.n = n;
   j.eps = eps;
   j.chi = chi;
+  j.W = p > kSmallP ? (cx<R>*)grow(E.W[slot], large_workspace_elems<R>(m, n) * sizeof(cx<R>))
+                    : nullptr;
   j.info = reinterpret_cast<int64_t*>(E.d_info->p) + 3 * slot;
   j.disc = reinterpret_cast<double*>(E.d_disc->p) + slot;
   if (p > E.counters[5]) E.counters[5] = p;

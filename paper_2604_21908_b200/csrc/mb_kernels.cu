@@ -727,13 +727,134 @@ __global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
   }
 }
 
+// ---- QR preconditioning (zgejsv-style) -----------------------------------
+// X0 (q x p, column-major) = Q R by Householder reflections (zgeqrf
+// conventions: v below the diagonal with implicit 1, beta on the diagonal).
+// One launch per column: every CTA owns whole trailing columns, forms
+// w_j = v^H x_j and x_j -= conj(tau) v w_j; the CTA that owns column k+1 then
+// builds the next reflector (look-ahead), so launch k+1 finds it ready.
+
+template <typename R>
+__device__ void make_reflector(cx<R>* __restrict__ col, int64_t k, int64_t q, cx<R>* tau_out,
+                               double* red) {
+  // col points at column k; rows k..q-1 are live
+  double acc = 0;
+  for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) acc += (double)cabs2(col[r]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int sft = blockDim.x / 2; sft > 0; sft >>= 1) {
+    if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
+    __syncthreads();
+  }
+  const double xn2 = red[0];
+  const cx<R> alpha = col[k];
+  __syncthreads();
+  if (xn2 == 0.0 && alpha.y == 0) {
+    if (threadIdx.x == 0) *tau_out = mk<R>(0, 0);
+    return;
+  }
+  const double an = sqrt((double)alpha.x * alpha.x + (double)alpha.y * alpha.y + xn2);
+  const double beta = alpha.x >= 0 ? -an : an;
+  // tau = (beta - alpha) / beta ; scale = 1 / (alpha - beta)
+  const double dr = (double)alpha.x - beta, di = (double)alpha.y;
+  const double den = dr * dr + di * di;
+  const cx<R> scale = mk<R>((R)(dr / den), (R)(-di / den));
+  for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) col[r] = cmul(col[r], scale);
+  if (threadIdx.x == 0) {
+    *tau_out = mk<R>((R)((beta - alpha.x) / beta), (R)(-alpha.y / beta));
+    col[k] = mk<R>((R)beta, 0);
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_qr_first(cx<R>* __restrict__ X, int64_t q,
+                                                 cx<R>* __restrict__ tau) {
+  __shared__ double red[256];
+  make_reflector<R>(X, 0, q, &tau[0], red);
+}
+
+// apply reflector k to columns k+1.. (each CTA: a strided set of columns)
+template <typename R>
+__global__ void __launch_bounds__(256) k_qr_step(cx<R>* __restrict__ X, int64_t q, int64_t p,
+                                                int64_t k, cx<R>* __restrict__ tau) {
+  __shared__ double red[256];
+  __shared__ cx<R> wj;
+  const cx<R> tk = tau[k];
+  const cx<R>* v = X + k * q;  // v[k] = 1 implicitly
+  for (int64_t j = k + 1 + blockIdx.x; j < p; j += gridDim.x) {
+    cx<R>* x = X + j * q;
+    if (!(tk.x == 0 && tk.y == 0)) {
+      // w = v^H x over rows k..q-1
+      double ax = 0, ay = 0;
+      for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
+        cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
+        cx<R> xr = x[r];
+        ax += (double)vr.x * xr.x + (double)vr.y * xr.y;
+        ay += (double)vr.x * xr.y - (double)vr.y * xr.x;
+      }
+      red[threadIdx.x] = ax;
+      __syncthreads();
+      for (int sft = 128; sft > 0; sft >>= 1) {
+        if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) wj.x = (R)red[0];
+      __syncthreads();
+      red[threadIdx.x] = ay;
+      __syncthreads();
+      for (int sft = 128; sft > 0; sft >>= 1) {
+        if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) wj.y = (R)red[0];
+      __syncthreads();
+      // x -= conj(tau) * v * w
+      const cx<R> f = cmul(cconj(tk), wj);
+      for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
+        cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
+        x[r] = csub(x[r], cmul(vr, f));
+      }
+      __syncthreads();
+    }
+    if (j == k + 1) make_reflector<R>(x, j, q, &tau[j], red);
+    __syncthreads();
+  }
+}
+
+// Z = R^H (p x p, column-major, lower triangular) from the QR'd X
+template <typename R>
+__global__ void k_make_z(const cx<R>* __restrict__ X, int64_t q, int64_t p, cx<R>* __restrict__ Z) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = e / p, i = e % p;  // Z(i, j) = conj(R(j, i)), R(j, i) = X[i*q + j] for j <= i
+    Z[e] = j <= i ? cconj(X[i * q + j]) : mk<R>(0, 0);
+  }
+}
+
+// U~ = Z' diag(1/sigma) (unsorted columns; zero-safe)
+template <typename R>
+__global__ void k_scale_cols(const cx<R>* __restrict__ Zr, const R* __restrict__ nrm, int64_t p,
+                             cx<R>* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    R s = nrm[e / p];
+    out[e] = s > 0 ? cscale(Zr[e], (R)1 / s) : mk<R>(0, 0);
+  }
+}
+
+template <typename R>
+size_t large_workspace_elems(int64_t m, int64_t n) {
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  return (size_t)(q * p + p * p + p);
+}
+
 static int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;
 }
 
 template <typename R, int W2, int CL>
-static void launch_round(const SvdJob<R>& J, int64_t p, int64_t q, int nb, int NB, int rnd,
+static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int NB, int rnd,
                          int* flag_dev, const double* fro2, int inner, cudaStream_t s) {
   size_t sm = sizeof(PairSmem<R, W2>);
   static bool attr = false;
@@ -742,56 +863,97 @@ static void launch_round(const SvdJob<R>& J, int64_t p, int64_t q, int nb, int N
                          (int)sm);
     attr = true;
   }
-  k_jacobi_pair_cl<R, W2, CL><<<(NB / 2) * CL, 256, sm, s>>>(J.X, J.V, p, q, nb, NB, rnd, flag_dev,
+  k_jacobi_pair_cl<R, W2, CL><<<(NB / 2) * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev,
                                                                fro2, inner);
   MB_LAUNCH_CHECK();
 }
 
+// Block one-sided Jacobi sweeps on the column-major Xw (p columns of length
+// len) until no pair rotates. Returns (converged, sweeps).
 template <typename R>
-void svd_large(const SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
-               cudaStream_t s) {
-  // block width and inner EVD sweeps per pair step (tunable for experiments)
+static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, int* flag_dev,
+                          int* flag_host, double* scratch_dev, cudaStream_t s, int& conv,
+                          int& sweeps) {
   static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : 32;
   static const int inner = env_int("MB_JACOBI_INNER", 1);
   static const int debug = env_int("MB_JACOBI_DEBUG", 0);
   const int w = W2 / 2;
-  const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
-  if (J.A) {
-    int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
-    k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n);
-    MB_LAUNCH_CHECK();
-  }
-  // ||A||_F^2 (rotation-invariant) for the backward-stability floor
+  // ||Xw||_F^2 (rotation-invariant) for the backward-stability floor
   double* fro2 = scratch_dev + kSumBlocks;
-  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, scratch_dev);
+  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(Xw, p * len, scratch_dev);
   MB_LAUNCH_CHECK();
   k_sumsq_final<<<1, 256, 0, s>>>(scratch_dev, kSumBlocks, fro2);
   MB_LAUNCH_CHECK();
   const int nb = (int)cdiv(p, w);
   const int NB = nb + (nb & 1);
   // 8-CTA clusters when the pairs alone cannot fill the chip
-  const bool wide = (NB / 2) * 4 < 148 && q >= 8 * 64;
-  int sweeps = 0, conv = 0;
-  for (; sweeps < 60; ++sweeps) {
+  const bool wide = (NB / 2) * 4 < 148 && len >= 8 * 64;
+  conv = 0;
+  for (sweeps = 0; sweeps < 60; ++sweeps) {
     cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
     for (int rnd = 0; rnd < NB - 1; ++rnd) {
       if (W2 == 64) {
-        if (wide) launch_round<R, 64, 8>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
-        else launch_round<R, 64, 4>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
+        if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+        else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
       } else {
-        if (wide) launch_round<R, 32, 8>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
-        else launch_round<R, 32, 4>(J, p, q, nb, NB, rnd, flag_dev, fro2, inner, s);
+        if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+        else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
       }
     }
     cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    if (debug) fprintf(stderr, "[svd_large p=%lld q=%lld] sweep %d rotated pairs %d of %d\n",
-                       (long long)p, (long long)q, sweeps, *flag_host, (NB / 2) * (NB - 1));
+    if (debug) fprintf(stderr, "[svd_large p=%lld len=%lld] sweep %d rotated pairs %d of %d\n",
+                       (long long)p, (long long)len, sweeps, *flag_host, (NB / 2) * (NB - 1));
     if (*flag_host == 0) { conv = 1; break; }
   }
-  // column norms into sig[p:2p] (the engine sizes sig for 2p), then sort into sig[0:p]
-  k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(J.X, p, q, J.sig + p);
-  MB_LAUNCH_CHECK();
+}
+
+template <typename R>
+void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev, cudaStream_t s) {
+  static const int precond = env_int("MB_JACOBI_QR", 1);
+  const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
+  if (J.A) {
+    int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
+    k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, precond ? nullptr : J.V, J.m, J.n);
+    MB_LAUNCH_CHECK();
+  }
+  int conv = 0, sweeps = 0;
+  if (!precond) {
+    jacobi_sweeps<R>(J.X, J.V, p, q, flag_dev, flag_host, scratch_dev, s, conv, sweeps);
+    k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(J.X, p, q, J.sig + p);
+    MB_LAUNCH_CHECK();
+  } else {
+    // 1. X0 = Q R (Householder, in the workspace copy)
+    cx<R>* Xq = J.W;
+    cx<R>* Z = J.W + q * p;
+    cx<R>* tau = Z + p * p;
+    cudaMemcpyAsync(Xq, J.X, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToDevice, s);
+    k_qr_first<R><<<1, 256, 0, s>>>(Xq, q, tau);
+    MB_LAUNCH_CHECK();
+    for (int64_t k = 0; k + 1 < p; ++k) {
+      int g = (int)std::min<int64_t>(p - k - 1, 148 * 4);
+      k_qr_step<R><<<g, 256, 0, s>>>(Xq, q, p, k, tau);
+      MB_LAUNCH_CHECK();
+    }
+    // 2. Z = R^H ; one-sided Jacobi on Z (p x p) without accumulating J
+    {
+      int blocks = (int)std::min<int64_t>(cdiv(p * p, 256), 148 * 16);
+      k_make_z<R><<<blocks, 256, 0, s>>>(Xq, q, p, Z);
+      MB_LAUNCH_CHECK();
+    }
+    jacobi_sweeps<R>(Z, nullptr, p, p, flag_dev, flag_host, scratch_dev, s, conv, sweeps);
+    // 3. sigma = column norms of Z J; U~ = Z J / sigma ; U*sigma = X0 U~
+    k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(Z, p, p, J.sig + p);
+    MB_LAUNCH_CHECK();
+    if (J.V) {
+      int blocks = (int)std::min<int64_t>(cdiv(p * p, 256), 148 * 16);
+      k_scale_cols<R><<<blocks, 256, 0, s>>>(Z, J.sig + p, p, J.V);
+      MB_LAUNCH_CHECK();
+      // row-major: (U sigma)^T (p x q) = U~^T (p x p) @ X0^T (p x q)
+      launch_gemm<R>(false, p, q, p, J.V, p, J.X, q, Xq, q, s);
+      J.X = Xq;
+    }
+  }
   k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
   MB_LAUNCH_CHECK();
   k_rank<R><<<1, 32, 0, s>>>(J, p, conv, sweeps + 1);
@@ -1068,7 +1230,8 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_gate1<R>(const cx<R>*, cx<R>*, const Gate2<R>&, int64_t, int64_t, bool,   \
                                 cudaStream_t);                                                  \
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
-  template void svd_large<R>(const SvdJob<R>&, int*, int*, double*, cudaStream_t);              \
+  template void svd_large<R>(SvdJob<R>&, int*, int*, double*, cudaStream_t);                    \
+  template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
   template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
                                cudaStream_t);                                                   \
   template void launch_identity<R>(cx<R>*, int64_t, cudaStream_t);                              \

@@ -22,6 +22,7 @@ struct SvdJob {
   int64_t chi;     // bond cap
   int64_t* info;   // [0]=kept rank, [1]=not-converged flag, [2]=sweeps
   double* disc;    // discarded weight
+  cx<R>* W;        // large path workspace: q*p (QR / final U*sigma) + p*p (R^H) + p (tau)
 };
 
 // Largest column count a single CTA factors on its own.
@@ -61,9 +62,13 @@ void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t 
 
 // Large SVD (p > kSmallP): host-driven block Jacobi sweeps. scratch_dev holds
 // >= 257 doubles (norm reduction).
+// (the job's X pointer is redirected to the workspace holding U*sigma)
 template <typename R>
-void svd_large(const SvdJob<R>& job, int* flag_dev, int* flag_host, double* scratch_dev,
+void svd_large(SvdJob<R>& job, int* flag_dev, int* flag_host, double* scratch_dev,
                cudaStream_t s);
+
+template <typename R>
+size_t large_workspace_elems(int64_t m, int64_t n);
 
 // Write truncated factors: Uout (m x k) = U[:, :k] (* sigma if scaleU),
 // Vout (k x n) = (sigma if scaleV *) Vh[:k, :]. Either pointer may be null.
