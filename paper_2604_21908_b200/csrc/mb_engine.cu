@@ -270,6 +270,20 @@ static double norm_of(const cx<R>* buf, int64_t n) {
 
 // ---- canonical-form plumbing (chains.py:110-145) ----------------------------
 
+// QR step of A (m x n row-major). right (push_right, m >= n): A = Q R, site = Q
+// (m x n), carry = R (n x n). left (push_left, m <= n): A^H = Q R, A = R^H Q^H,
+// site = Q^H (m x n, orthonormal rows), carry = L = R^H (m x m).
+template <typename R>
+static void qr_step(const cx<R>* A, int64_t m, int64_t n, bool right, cx<R>* site, cx<R>* carry) {
+  const int64_t p = right ? n : m, q = right ? m : n;
+  cx<R>* X = (cx<R>*)grow(E.X[0], (size_t)(p * q) * sizeof(cx<R>));
+  cx<R>* Y = (cx<R>*)grow(E.W[0], (size_t)(p * q + p) * sizeof(cx<R>));
+  ProfScope ps(P_SVD_LARGE, 8.0 * 2.0 * (double)q * (double)p * (double)p);
+  launch_to_x<R>(A, X, m, n, !right, E.stream);
+  qr_explicit<R>(X, Y, Y + p * q, q, p, E.stream);
+  launch_qr_emit<R>(Y, X, q, p, right, site, carry, E.stream);
+}
+
 // Left-orthogonalize site i, pushing the remainder into site i+1 (chains.py:110).
 template <typename R>
 static void push_right(mb_chain& c, int i) {
@@ -285,6 +299,12 @@ static void push_right(mb_chain& c, int i) {
     }
     nB = new_site<R>(m, d, B.r);
     gemm<R>(false, m, rn, n, P<R>(A), n, P<R>(B), rn, P<R>(nB), rn);
+  } else if (n > kSmallP) {  // Householder QR, as numpy's reduced qr (chains.py:113)
+    nA = new_site<R>(A.l, d, n);
+    cx<R>* Rm = (cx<R>*)grow(E.carry, (size_t)(n * n) * sizeof(cx<R>));
+    qr_step<R>(P<R>(A), m, n, true, P<R>(nA), Rm);
+    nB = new_site<R>(n, d, B.r);
+    gemm<R>(false, n, rn, n, Rm, n, P<R>(B), rn, P<R>(nB), rn);
   } else {
     SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
     run_jobs<R>(&j, 1);
@@ -313,6 +333,12 @@ static void push_left(mb_chain& c, int i) {
     }
     nP = new_site<R>(Pv.l, d, n);
     gemm<R>(false, pm, n, m, P<R>(Pv), m, P<R>(A), n, P<R>(nP), n);
+  } else if (m > kSmallP) {  // LQ through Householder QR of A^H (chains.py:123)
+    nA = new_site<R>(m, d, A.r);
+    cx<R>* L = (cx<R>*)grow(E.carry, (size_t)(m * m) * sizeof(cx<R>));
+    qr_step<R>(P<R>(A), m, n, false, P<R>(nA), L);
+    nP = new_site<R>(Pv.l, d, m);
+    gemm<R>(false, pm, m, m, P<R>(Pv), m, L, m, P<R>(nP), m);
   } else {
     SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
     run_jobs<R>(&j, 1);

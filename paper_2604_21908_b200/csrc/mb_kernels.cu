@@ -842,6 +842,72 @@ __global__ void k_scale_cols(const cx<R>* __restrict__ Zr, const R* __restrict__
   }
 }
 
+// Explicit Q (q x p, column-major) by backward accumulation:
+// Y = [I; 0]; for k = p-1..0: Y[k:, k:] <- H_k Y[k:, k:], H_k = I - tau v v^H.
+template <typename R>
+__global__ void k_q_init(cx<R>* __restrict__ Y, int64_t q, int64_t p) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q * p;
+       e += (int64_t)gridDim.x * blockDim.x)
+    Y[e] = mk<R>((e % q) == (e / q) ? 1 : 0, 0);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_q_step(const cx<R>* __restrict__ X, cx<R>* __restrict__ Y,
+                                               int64_t q, int64_t p, int64_t k,
+                                               const cx<R>* __restrict__ tau) {
+  __shared__ double red[2][256];
+  const cx<R> tk = tau[k];
+  if (tk.x == 0 && tk.y == 0) return;
+  const cx<R>* v = X + k * q;
+  for (int64_t j = k + blockIdx.x; j < p; j += gridDim.x) {
+    cx<R>* y = Y + j * q;
+    double ax = 0, ay = 0;
+    for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
+      cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
+      cx<R> yr = y[r];
+      ax += (double)vr.x * yr.x + (double)vr.y * yr.y;
+      ay += (double)vr.x * yr.y - (double)vr.y * yr.x;
+    }
+    red[0][threadIdx.x] = ax;
+    red[1][threadIdx.x] = ay;
+    __syncthreads();
+    for (int sft = 128; sft > 0; sft >>= 1) {
+      if (threadIdx.x < sft) {
+        red[0][threadIdx.x] += red[0][threadIdx.x + sft];
+        red[1][threadIdx.x] += red[1][threadIdx.x + sft];
+      }
+      __syncthreads();
+    }
+    const cx<R> f = cmul(tk, mk<R>((R)red[0][0], (R)red[1][0]));
+    for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
+      cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
+      y[r] = csub(y[r], cmul(vr, f));
+    }
+    __syncthreads();
+  }
+}
+
+// Householder QR of the column-major X (q x p, q >= p) in place (R in the
+// upper triangle, reflectors below) plus explicit Q into Y (q x p).
+template <typename R>
+void qr_explicit(cx<R>* X, cx<R>* Y, cx<R>* tau, int64_t q, int64_t p, cudaStream_t s) {
+  k_qr_first<R><<<1, 256, 0, s>>>(X, q, tau);
+  MB_LAUNCH_CHECK();
+  for (int64_t k = 0; k + 1 < p; ++k) {
+    int g = (int)std::min<int64_t>(p - k - 1, 148 * 4);
+    k_qr_step<R><<<g, 256, 0, s>>>(X, q, p, k, tau);
+    MB_LAUNCH_CHECK();
+  }
+  int blocks = (int)std::min<int64_t>(cdiv(q * p, 256), 148 * 16);
+  k_q_init<R><<<blocks, 256, 0, s>>>(Y, q, p);
+  MB_LAUNCH_CHECK();
+  for (int64_t k = p - 1; k >= 0; --k) {
+    int g = (int)std::min<int64_t>(p - k, 148 * 4);
+    k_q_step<R><<<g, 256, 0, s>>>(X, Y, q, p, k, tau);
+    MB_LAUNCH_CHECK();
+  }
+}
+
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n) {
   const int64_t p = m < n ? m : n, q = m < n ? n : m;
@@ -910,7 +976,12 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, int* fla
 
 template <typename R>
 void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev, cudaStream_t s) {
-  static const int precond = env_int("MB_JACOBI_QR", 1);
+  // QR preconditioning is used for values-only problems and for truncations at
+  // cutoffs >= 1e-6, where every kept singular value sits far above the noise
+  // floor so U~ = Z J / sigma is accurate. Tighter cutoffs (which keep
+  // noise-level columns) use the plain path, whose J is unitary by construction.
+  static const int allow_pre = env_int("MB_JACOBI_QR", 1);
+  const int precond = allow_pre && (J.V == nullptr || J.eps >= 1e-6);
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   if (J.A) {
     int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
@@ -957,6 +1028,59 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
   k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
   MB_LAUNCH_CHECK();
   k_rank<R><<<1, 32, 0, s>>>(J, p, conv, sweeps + 1);
+  MB_LAUNCH_CHECK();
+}
+
+// QR-step outputs. Q (q x p col-major) / R (upper triangle of the QR'd X).
+//  tall (push_right, X = A):   site = Q as row-major (q x p); carry = R row-major (p x p)
+//  wide (push_left,  X = A^H): site = Q^H row-major (p x q);  carry = R^H row-major (p x p)
+template <typename R>
+__global__ void k_qr_emit(const cx<R>* __restrict__ Q, const cx<R>* __restrict__ Xr, int64_t q,
+                          int64_t p, bool tall, cx<R>* __restrict__ site, cx<R>* __restrict__ carry) {
+  const int64_t ns = q * p, nc = p * p;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ns + nc;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < ns) {
+      if (tall) {
+        int64_t r = e / p, c = e % p;  // site[r][c] = Q(r, c)
+        site[e] = Q[c * q + r];
+      } else {
+        int64_t r = e / q, c = e % q;  // site[r][c] = conj(Q(c, r))
+        site[e] = cconj(Q[r * q + c]);
+      }
+    } else {
+      int64_t f = e - ns, r = f / p, c = f % p;
+      if (tall) carry[f] = r <= c ? Xr[c * q + r] : mk<R>(0, 0);          // R(r, c)
+      else carry[f] = c <= r ? cconj(Xr[r * q + c]) : mk<R>(0, 0);         // conj(R(c, r))
+    }
+  }
+}
+
+template <typename R>
+void launch_qr_emit(const cx<R>* Q, const cx<R>* Xr, int64_t q, int64_t p, bool tall, cx<R>* site,
+                    cx<R>* carry, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(q * p + p * p, 256), 148 * 16);
+  k_qr_emit<R><<<blocks, 256, 0, s>>>(Q, Xr, q, p, tall, site, carry);
+  MB_LAUNCH_CHECK();
+}
+
+template <typename R>
+__global__ void k_to_x(const cx<R>* __restrict__ A, cx<R>* __restrict__ X, int64_t m, int64_t n,
+                       bool herm) {
+  const int64_t tot = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (herm) X[e] = cconj(A[e]);           // column j of X = conj(row j of A), length n
+    else X[(e % n) * m + e / n] = A[e];     // column j of X = column j of A, length m
+  }
+}
+
+// A (m x n row-major) -> column-major working X: X = A (tall, q = m) or A^H
+// (herm, q = n)
+template <typename R>
+void launch_to_x(const cx<R>* A, cx<R>* X, int64_t m, int64_t n, bool herm, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>(cdiv(m * n, 256), 148 * 32);
+  k_to_x<R><<<blocks, 256, 0, s>>>(A, X, m, n, herm);
   MB_LAUNCH_CHECK();
 }
 
@@ -1232,6 +1356,10 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
   template void svd_large<R>(SvdJob<R>&, int*, int*, double*, cudaStream_t);                    \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
+  template void qr_explicit<R>(cx<R>*, cx<R>*, cx<R>*, int64_t, int64_t, cudaStream_t);        \
+  template void launch_qr_emit<R>(const cx<R>*, const cx<R>*, int64_t, int64_t, bool, cx<R>*,   \
+                                  cx<R>*, cudaStream_t);                                        \
+  template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
   template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
                                cudaStream_t);                                                   \
   template void launch_identity<R>(cx<R>*, int64_t, cudaStream_t);                              \

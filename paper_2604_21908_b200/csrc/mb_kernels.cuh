@@ -70,6 +70,21 @@ void svd_large(SvdJob<R>& job, int* flag_dev, int* flag_host, double* scratch_de
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n);
 
+// Householder QR (zgeqrf conventions) of the column-major X (q x p) in place,
+// explicit Q into Y; tau needs p entries.
+template <typename R>
+void qr_explicit(cx<R>* X, cx<R>* Y, cx<R>* tau, int64_t q, int64_t p, cudaStream_t s);
+
+// site/carry of a QR step from (Q, R): tall = push_right (site Q, carry R),
+// wide = push_left (site Q^H, carry R^H = L), all row-major.
+template <typename R>
+void launch_qr_emit(const cx<R>* Q, const cx<R>* Xr, int64_t q, int64_t p, bool tall, cx<R>* site,
+                    cx<R>* carry, cudaStream_t s);
+
+// A (m x n row-major) -> column-major working X: A itself (q = m) or A^H (herm, q = n)
+template <typename R>
+void launch_to_x(const cx<R>* A, cx<R>* X, int64_t m, int64_t n, bool herm, cudaStream_t s);
+
 // Write truncated factors: Uout (m x k) = U[:, :k] (* sigma if scaleU),
 // Vout (k x n) = (sigma if scaleV *) Vh[:k, :]. Either pointer may be null.
 template <typename R>

@@ -154,6 +154,40 @@ def test_interleaved_left_right_and_compress():
         np.testing.assert_allclose(mpo_to_dense(m2), dense, atol=1e-9)
 
 
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_large_bond_qr_steps_and_compress(dtype):
+    """Bonds > 64 route center moves through the Householder QR kernels and
+    truncations through the QR-preconditioned Jacobi path."""
+    rng = np.random.default_rng(77)
+    bonds = [1, 4, 16, 64, 100, 64, 16, 4, 1]
+    sites = [(rng.standard_normal((bonds[i], 2, 2, bonds[i + 1]))
+              + 1j * rng.standard_normal((bonds[i], 2, 2, bonds[i + 1]))) / np.sqrt(bonds[i])
+             for i in range(8)]
+    m = MatrixProductOperator.from_sites(sites, dtype=dtype)
+    oc = mo.OChain(tuple(sites), 0.0, None)
+    dense = mo.chain_dense(oc)
+    tol = 1e-9 if dtype == "complex128" else 2e-4
+    scale = np.abs(dense).max()
+    for target in (7, 0, 4, 3):
+        m = move_center(m, target)
+        np.testing.assert_allclose(mpo_to_dense(m), dense, atol=tol * scale)
+        for i, s_ in enumerate(m.sites):  # canonical form around the center
+            if i < target:
+                mat = s_.reshape(-1, s_.shape[-1])
+                np.testing.assert_allclose(mat.conj().T @ mat, np.eye(mat.shape[1]), atol=10 * tol)
+            elif i > target:
+                mat = s_.reshape(s_.shape[0], -1)
+                np.testing.assert_allclose(mat @ mat.conj().T, np.eye(mat.shape[0]), atol=10 * tol)
+    for eps in (0.0, 2e-3):
+        mc, occ = compress(m, eps, 10**6), mo.compress(oc, eps, 10**6)
+        if dtype == "complex128":
+            assert mc.bond_dims() == occ.bonds()
+            assert mc.log_norm == pytest.approx(occ.log_norm, abs=1e-9)
+        ref = mo.chain_dense(occ)
+        err = np.linalg.norm(mpo_to_dense(mc) - ref) / np.linalg.norm(ref)
+        assert err < (1e-9 if dtype == "complex128" else 1e-4)
+
+
 def test_swap_boundary_cases():
     sw = Gate("swap", (0, 1))
     m = absorb_gate(identity_mpo(2), sw, "left", EXACT, 64)
