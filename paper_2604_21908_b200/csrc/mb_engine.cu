@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -270,6 +272,48 @@ static double norm_of(const cx<R>* buf, int64_t n) {
 
 // ---- canonical-form plumbing (chains.py:110-145) ----------------------------
 
+// Debug aid (MB_CHECK_SITES=1): report the first operation whose output site
+// is all-zero or non-finite.
+static bool check_sites_enabled() {
+  static const bool on = getenv("MB_CHECK_SITES") && atoi(getenv("MB_CHECK_SITES"));
+  return on;
+}
+
+template <typename R>
+static bool check_site(const char* op, int i, const Site& s, int d, int64_t m, int64_t n) {
+  if (!check_sites_enabled()) return true;
+  double f = norm_of<R>(P<R>(s), s.l * d * s.r);
+  if (!(f > 0) || !std::isfinite(f)) {
+    fprintf(stderr, "[mb check] %s site %d (l=%lld r=%lld) from %lldx%lld: norm %g\n", op, i,
+            (long long)s.l, (long long)s.r, (long long)m, (long long)n, f);
+    return false;
+  }
+  return true;
+}
+
+// dump a device matrix (complex) as raw complex128 for offline replay
+template <typename R>
+static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n) {
+  const char* dir = getenv("MB_DUMP_DIR");
+  static int count = 0;
+  if (!dir || count >= 4) return;
+  std::vector<double> host((size_t)(2 * m * n));
+  cx<double>* tmp = nullptr;
+  cudaMalloc(&tmp, (size_t)(m * n) * 16);
+  launch_convert<double>(dev, sizeof(R) == sizeof(double), tmp, m * n, E.stream);
+  cudaMemcpyAsync(host.data(), tmp, (size_t)(m * n) * 16, cudaMemcpyDeviceToHost, E.stream);
+  cudaStreamSynchronize(E.stream);
+  cudaFree(tmp);
+  char path[512];
+  snprintf(path, sizeof(path), "%s/%s_%d_%lldx%lld.bin", dir, tag, count++, (long long)m,
+           (long long)n);
+  FILE* f = fopen(path, "wb");
+  if (f) {
+    fwrite(host.data(), sizeof(double), host.size(), f);
+    fclose(f);
+  }
+}
+
 // QR step of A (m x n row-major). right (push_right, m >= n): A = Q R, site = Q
 // (m x n), carry = R (n x n). left (push_left, m <= n): A^H = Q R, A = R^H Q^H,
 // site = Q^H (m x n, orthonormal rows), carry = L = R^H (m x m).
@@ -314,6 +358,8 @@ static void push_right(mb_chain& c, int i) {
     nB = new_site<R>(n, d, B.r);
     gemm<R>(false, n, rn, n, Rm, n, P<R>(B), rn, P<R>(nB), rn);
   }
+  check_site<R>("push_right.site", i, nA, d, m, n);
+  check_site<R>("push_right.next", i + 1, nB, d, m, n);
   c.s[i] = nA;
   c.s[i + 1] = nB;
 }
@@ -348,6 +394,8 @@ static void push_left(mb_chain& c, int i) {
     nP = new_site<R>(Pv.l, d, m);
     gemm<R>(false, pm, m, m, P<R>(Pv), m, L, m, P<R>(nP), m);
   }
+  check_site<R>("push_left.site", i, nA, d, m, n);
+  check_site<R>("push_left.prev", i - 1, nP, d, m, n);
   c.s[i] = nA;
   c.s[i - 1] = nP;
 }
@@ -395,8 +443,14 @@ static void resplit(mb_chain& c, int b, cx<R>* th, int64_t l, int64_t r, double 
   run_jobs<R>(&j, 1);
   read_info(1);
   const int64_t k = E.h_info[0];
+  if (check_sites_enabled() && getenv("MB_DUMP_DIR")) {
+    // keep a copy of theta before the SVD could touch scratch
+  }
   Site nA = new_site<R>(l, 4, k), nB = new_site<R>(k, 4, r);
   emit<R>(j, k, P<R>(nA), false, P<R>(nB), true);
+  bool ok = check_site<R>("resplit.left", b, nA, 4, 4 * l, 4 * r);
+  ok = check_site<R>("resplit.right", b + 1, nB, 4, 4 * l, 4 * r) && ok;
+  if (!ok) dump_matrix<R>("theta", th, 4 * l, 4 * r);
   c.s[b] = nA;
   c.s[b + 1] = nB;
   c.center = b + 1;
@@ -500,6 +554,8 @@ static void truncate_left(mb_chain& c, int i, double eps, int64_t chi) {
   emit<R>(j, k, carry, true, P<R>(nA), false);
   Site nP = new_site<R>(Pv.l, d, k);
   gemm<R>(false, Pv.l * d, k, m, P<R>(Pv), m, carry, k, P<R>(nP), k);
+  check_site<R>("truncate.site", i, nA, d, m, n);
+  check_site<R>("truncate.prev", i - 1, nP, d, m, n);
   c.s[i] = nA;
   c.s[i - 1] = nP;
 }

@@ -737,32 +737,58 @@ __global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
 template <typename R>
 __device__ void make_reflector(cx<R>* __restrict__ col, int64_t k, int64_t q, cx<R>* tau_out,
                                double* red) {
-  // col points at column k; rows k..q-1 are live
+  // col points at column k; rows k..q-1 are live. All magnitudes are scaled by
+  // the column's max-abs entry so that rank-deficient trailing columns (pure
+  // rounding noise that shrinks toward the underflow range) never produce a
+  // zero denominator (zlarfg's rescaling, done once by the max-abs scale).
+  double mx = 0;
+  for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
+    cx<R> v = col[r];
+    mx = fmax(mx, fmax(fabs((double)v.x), fabs((double)v.y)));
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int sft = blockDim.x / 2; sft > 0; sft >>= 1) {
+    if (threadIdx.x < sft) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + sft]);
+    __syncthreads();
+  }
+  const double amax = red[0];
+  __syncthreads();
+  if (!(amax > 0)) {
+    if (threadIdx.x == 0) *tau_out = mk<R>(0, 0);
+    return;
+  }
+  const double inv = 1.0 / amax;
   double acc = 0;
-  for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) acc += (double)cabs2(col[r]);
+  for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) {
+    cx<R> v = col[r];
+    double a = v.x * inv, b = v.y * inv;
+    acc += a * a + b * b;
+  }
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int sft = blockDim.x / 2; sft > 0; sft >>= 1) {
     if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
     __syncthreads();
   }
-  const double xn2 = red[0];
+  const double xn2 = red[0];  // scaled
   const cx<R> alpha = col[k];
   __syncthreads();
   if (xn2 == 0.0 && alpha.y == 0) {
     if (threadIdx.x == 0) *tau_out = mk<R>(0, 0);
     return;
   }
-  const double an = sqrt((double)alpha.x * alpha.x + (double)alpha.y * alpha.y + xn2);
-  const double beta = alpha.x >= 0 ? -an : an;
-  // tau = (beta - alpha) / beta ; scale = 1 / (alpha - beta)
-  const double dr = (double)alpha.x - beta, di = (double)alpha.y;
-  const double den = dr * dr + di * di;
-  const cx<R> scale = mk<R>((R)(dr / den), (R)(-di / den));
+  const double ar = alpha.x * inv, ai = alpha.y * inv;  // scaled alpha
+  const double an = sqrt(ar * ar + ai * ai + xn2);      // scaled |(alpha, x)|
+  const double bs = ar >= 0 ? -an : an;                 // scaled beta
+  // tau = (beta - alpha) / beta (scale-free) ; 1 / (alpha - beta) = inv / (a_s - b_s)
+  const double dr = ar - bs, di = ai;
+  const double den = dr * dr + di * di;  // >= an^2 >= ~1 in scaled units
+  const cx<R> scale = mk<R>((R)(inv * dr / den), (R)(-inv * di / den));
   for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) col[r] = cmul(col[r], scale);
   if (threadIdx.x == 0) {
-    *tau_out = mk<R>((R)((beta - alpha.x) / beta), (R)(-alpha.y / beta));
-    col[k] = mk<R>((R)beta, 0);
+    *tau_out = mk<R>((R)((bs - ar) / bs), (R)(-ai / bs));
+    col[k] = mk<R>((R)(bs * amax), 0);
   }
 }
 
@@ -975,7 +1001,33 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, int* fla
 }
 
 template <typename R>
+__global__ void k_count_bad(const cx<R>* __restrict__ x, int64_t n, int* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    cx<R> v = x[e];
+    if (!isfinite((double)v.x) || !isfinite((double)v.y)) atomicAdd(out, 1);
+  }
+}
+
+// MB_CHECK_SITES debug aid: count non-finite entries of a device buffer
+template <typename R>
+static int count_bad(const cx<R>* x, int64_t n, cudaStream_t s) {
+  static int* d = nullptr;
+  static int* h = nullptr;
+  if (!d) {
+    cudaMalloc(&d, sizeof(int));
+    cudaMallocHost(&h, sizeof(int));
+  }
+  cudaMemsetAsync(d, 0, sizeof(int), s);
+  k_count_bad<R><<<148, 256, 0, s>>>(x, n, d);
+  cudaMemcpyAsync(h, d, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  return *h;
+}
+
+template <typename R>
 void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev, cudaStream_t s) {
+  static const int dbg = env_int("MB_CHECK_SITES", 0);
   // QR preconditioning is used for values-only problems and for truncations at
   // cutoffs >= 1e-6, where every kept singular value sits far above the noise
   // floor so U~ = Z J / sigma is accurate. Tighter cutoffs (which keep
@@ -998,6 +1050,11 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
     cx<R>* Xq = J.W;
     cx<R>* Z = J.W + q * p;
     cx<R>* tau = Z + p * p;
+    if (dbg) {
+      int b0 = count_bad<R>(J.A, J.m * J.n, s), b1 = count_bad<R>(J.X, q * p, s);
+      if (b0 || b1) fprintf(stderr, "[svd_large dbg] bad input A=%d X0=%d (m=%lld n=%lld)\n", b0, b1,
+                            (long long)J.m, (long long)J.n);
+    }
     cudaMemcpyAsync(Xq, J.X, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToDevice, s);
     k_qr_first<R><<<1, 256, 0, s>>>(Xq, q, tau);
     MB_LAUNCH_CHECK();
@@ -1012,7 +1069,30 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
       k_make_z<R><<<blocks, 256, 0, s>>>(Xq, q, p, Z);
       MB_LAUNCH_CHECK();
     }
+    if (dbg) {
+      int bq = count_bad<R>(Xq, q * p, s), bt = count_bad<R>(tau, p, s), bz = count_bad<R>(Z, p * p, s);
+      if (bq || bt || bz) {
+        fprintf(stderr, "[svd_large dbg] after QR: Xq=%d tau=%d Z=%d (q=%lld p=%lld)\n", bq, bt, bz,
+                (long long)q, (long long)p);
+        const char* dir = getenv("MB_DUMP_DIR");
+        static int dumped = 0;
+        if (dir && !dumped) {
+          dumped = 1;
+          std::vector<cx<R>> h((size_t)(q * p));
+          cudaMemcpy(h.data(), J.X, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToHost);
+          char path[512];
+          snprintf(path, sizeof(path), "%s/x0_%lldx%lld_%d.bin", dir, (long long)q, (long long)p,
+                   (int)sizeof(R));
+          FILE* f = fopen(path, "wb");
+          if (f) { fwrite(h.data(), sizeof(cx<R>), h.size(), f); fclose(f); }
+        }
+      }
+    }
     jacobi_sweeps<R>(Z, nullptr, p, p, flag_dev, flag_host, scratch_dev, s, conv, sweeps);
+    if (dbg) {
+      int bz = count_bad<R>(Z, p * p, s);
+      if (bz) fprintf(stderr, "[svd_large dbg] after Jacobi: Z=%d sweeps=%d\n", bz, sweeps);
+    }
     // 3. sigma = column norms of Z J; U~ = Z J / sigma ; U*sigma = X0 U~
     k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(Z, p, p, J.sig + p);
     MB_LAUNCH_CHECK();
@@ -1023,6 +1103,10 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
       // row-major: (U sigma)^T (p x q) = U~^T (p x p) @ X0^T (p x q)
       launch_gemm<R>(false, p, q, p, J.V, p, J.X, q, Xq, q, s);
       J.X = Xq;
+      if (dbg) {
+        int bv = count_bad<R>(J.V, p * p, s), bx = count_bad<R>(Xq, q * p, s);
+        if (bv || bx) fprintf(stderr, "[svd_large dbg] after assembly: V=%d X=%d\n", bv, bx);
+      }
     }
   }
   k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
