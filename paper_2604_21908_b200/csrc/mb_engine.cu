@@ -314,6 +314,13 @@ static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n)
   }
 }
 
+// Center moves through the explicit-Q Householder kernels (2p launches) are
+// opt-in (MB_QR_STEPS=1); by default they use the SVD split (same shapes).
+static bool use_qr_steps() {
+  static const bool on = getenv("MB_QR_STEPS") && atoi(getenv("MB_QR_STEPS"));
+  return on;
+}
+
 // QR step of A (m x n row-major). right (push_right, m >= n): A = Q R, site = Q
 // (m x n), carry = R (n x n). left (push_left, m <= n): A^H = Q R, A = R^H Q^H,
 // site = Q^H (m x n, orthonormal rows), carry = L = R^H (m x m).
@@ -343,7 +350,7 @@ static void push_right(mb_chain& c, int i) {
     }
     nB = new_site<R>(m, d, B.r);
     gemm<R>(false, m, rn, n, P<R>(A), n, P<R>(B), rn, P<R>(nB), rn);
-  } else if (n > kSmallP) {  // Householder QR, as numpy's reduced qr (chains.py:113)
+  } else if (n > kSmallP && use_qr_steps()) {  // Householder QR (chains.py:113)
     nA = new_site<R>(A.l, d, n);
     cx<R>* Rm = (cx<R>*)grow(E.carry, (size_t)(n * n) * sizeof(cx<R>));
     qr_step<R>(P<R>(A), m, n, true, P<R>(nA), Rm);
@@ -379,7 +386,7 @@ static void push_left(mb_chain& c, int i) {
     }
     nP = new_site<R>(Pv.l, d, n);
     gemm<R>(false, pm, n, m, P<R>(Pv), m, P<R>(A), n, P<R>(nP), n);
-  } else if (m > kSmallP) {  // LQ through Householder QR of A^H (chains.py:123)
+  } else if (m > kSmallP && use_qr_steps()) {  // LQ via Householder QR of A^H (chains.py:123)
     nA = new_site<R>(m, d, A.r);
     cx<R>* L = (cx<R>*)grow(E.carry, (size_t)(m * m) * sizeof(cx<R>));
     qr_step<R>(P<R>(A), m, n, false, P<R>(nA), L);

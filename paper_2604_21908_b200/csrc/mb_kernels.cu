@@ -754,7 +754,11 @@ __device__ void make_reflector(cx<R>* __restrict__ col, int64_t k, int64_t q, cx
   }
   const double amax = red[0];
   __syncthreads();
-  if (!(amax > 0)) {
+  // Columns below the safe minimum are rounding noise that has decayed through
+  // the trailing reflections (down to denormals); 1/amax would overflow, and
+  // H = I is exact to that precision.
+  const double safmin = sizeof(R) == sizeof(double) ? 1e-150 : 1e-18;
+  if (!(amax > safmin)) {
     if (threadIdx.x == 0) *tau_out = mk<R>(0, 0);
     return;
   }
@@ -1078,8 +1082,16 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
         static int dumped = 0;
         if (dir && !dumped) {
           dumped = 1;
-          std::vector<cx<R>> h((size_t)(q * p));
+          std::vector<cx<R>> h((size_t)(q * p)), hq((size_t)(q * p)), ht((size_t)p);
           cudaMemcpy(h.data(), J.X, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToHost);
+          cudaMemcpy(hq.data(), Xq, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToHost);
+          cudaMemcpy(ht.data(), tau, sizeof(cx<R>) * (size_t)p, cudaMemcpyDeviceToHost);
+          {
+            char pq[512];
+            snprintf(pq, sizeof(pq), "%s/xq_%lldx%lld_%d.bin", dir, (long long)q, (long long)p, (int)sizeof(R));
+            FILE* g = fopen(pq, "wb");
+            if (g) { fwrite(hq.data(), sizeof(cx<R>), hq.size(), g); fwrite(ht.data(), sizeof(cx<R>), ht.size(), g); fclose(g); }
+          }
           char path[512];
           snprintf(path, sizeof(path), "%s/x0_%lldx%lld_%d.bin", dir, (long long)q, (long long)p,
                    (int)sizeof(R));
