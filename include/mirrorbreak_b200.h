@@ -112,7 +112,13 @@ int mb_peak(const mb_chain* psi, uint8_t* bits, double* probs);
  * (site-major, the reference's rng.random(shots) per site); bits: shots x n. */
 int mb_sample(const mb_chain* psi, int64_t shots, const double* uniforms, uint8_t* bits);
 
-/* ---- dense tensor primitive ------------------------------------------- */
+/* ---- dense tensor primitives ------------------------------------------ */
+/* C (m x n) = A (m x k) . B (k x n), complex, host buffers (interleaved
+ * complex128). dtype MB_C64 with tensor_cores=1 runs the tcgen05 kind::tf32
+ * kernel (3xTF32 split); otherwise the CUDA-core kernel. Pair-blob
+ * contraction of chains.py:170 (numpy tensordot). */
+int mb_gemm(const double* a, const double* b, int64_t m, int64_t n, int64_t k, int dtype,
+            int tensor_cores, double* c);
 /* Truncated SVD of a host m x n complex128 matrix computed on the device
  * (tensor.py:84-116). Writes u (m x k), s (k), v (k x n) for the kept rank k
  * (buffers sized for min(m, n)); *rank = k; *discarded = relative discarded

@@ -64,6 +64,7 @@ _SIGS = {
     "mb_peak": (_i, [_p, _u8p, _dp]),
     "mb_sample": (_i, [_p, _i64, _dp, _u8p]),
     "mb_svd_truncate": (_i, [_dp, _i64, _i64, _i, _d, _i64, _dp, _dp, _dp, _i64p, _dp]),
+    "mb_gemm": (_i, [_dp, _dp, _i64, _i64, _i64, _i, _i, _dp]),
 }
 
 

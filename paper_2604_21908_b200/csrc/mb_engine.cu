@@ -67,7 +67,7 @@ struct Engine {
   // grow-only scratch
   static constexpr int kSlots = 4;
   Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots], W[kSlots];
-  Buf carry, env[2], amp, misc;
+  Buf carry, env[2], amp, misc, tcws;
   long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [6] h2d bytes, [7] d2h bytes
   // profiling
   bool prof = false;
@@ -176,10 +176,24 @@ static void require(bool ok, const char* msg) {
 
 static double gemm_flops(int64_t M, int64_t N, int64_t K) { return 8.0 * M * N * K; }
 
+// complex64 GEMMs big enough to fill 128x128 tensor-core tiles go to the
+// tcgen05 kernel (MB_TC=0 disables); everything else on the CUDA-core tiles.
+static bool tc_enabled() {
+  static const bool on = !getenv("MB_TC") || atoi(getenv("MB_TC")) != 0;
+  return on;
+}
+
 template <typename R>
 static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64_t lda,
                  const cx<R>* B, int64_t ldb, cx<R>* C, int64_t ldc) {
   ProfScope ps(P_GEMM, gemm_flops(M, N, K));
+  if (sizeof(R) == sizeof(float) && !ct && tc_enabled() && M >= 128 && N >= 64 && K >= 16 &&
+      M * N * K >= (int64_t)1 << 21) {
+    void* ws = grow(E.tcws, tc_workspace_bytes(M, N, K));
+    tc_gemm_c64(M, N, K, (const cx<float>*)A, lda, (const cx<float>*)B, ldb, (cx<float>*)C, ldc,
+                ws, E.stream);
+    return;
+  }
   launch_gemm<R>(ct, M, N, K, A, lda, B, ldb, C, ldc, E.stream);
 }
 
@@ -1061,6 +1075,42 @@ int mb_sample(const mb_chain* psi, int64_t shots, const double* uniforms, uint8_
   MB_TRY({
     if (psi->dtype == MB_C64) sample<float>(*psi, shots, uniforms, bits);
     else sample<double>(*psi, shots, uniforms, bits);
+    return 0;
+  });
+}
+
+int mb_gemm(const double* a, const double* b, int64_t m, int64_t n, int64_t k, int dtype,
+            int tensor_cores, double* c) {
+  MB_TRY({
+    ensure_ready();
+    require(m >= 1 && n >= 1 && k >= 1, "empty gemm");
+    if (dtype == MB_C64) {
+      Buf dA = alloc((size_t)(m * k) * 8);
+      Buf dB = alloc((size_t)(k * n) * 8);
+      Buf dC = alloc((size_t)(m * n) * 8);
+      upload<float>(a, (cx<float>*)dA->p, m * k);
+      upload<float>(b, (cx<float>*)dB->p, k * n);
+      if (tensor_cores) {
+        void* ws = grow(E.tcws, tc_workspace_bytes(m, n, k));
+        tc_gemm_c64(m, n, k, (cx<float>*)dA->p, k, (cx<float>*)dB->p, n, (cx<float>*)dC->p, n, ws,
+                    E.stream);
+      } else {
+        launch_gemm<float>(false, m, n, k, (cx<float>*)dA->p, k, (cx<float>*)dB->p, n,
+                           (cx<float>*)dC->p, n, E.stream);
+      }
+      download<float>((cx<float>*)dC->p, c, m * n);
+    } else {
+      require(!tensor_cores, "tensor-core path is complex64 only");
+      Buf dA = alloc((size_t)(m * k) * 16);
+      Buf dB = alloc((size_t)(k * n) * 16);
+      Buf dC = alloc((size_t)(m * n) * 16);
+      upload<double>(a, (cx<double>*)dA->p, m * k);
+      upload<double>(b, (cx<double>*)dB->p, k * n);
+      launch_gemm<double>(false, m, n, k, (cx<double>*)dA->p, k, (cx<double>*)dB->p, n,
+                          (cx<double>*)dC->p, n, E.stream);
+      download<double>((cx<double>*)dC->p, c, m * n);
+    }
+    sync();
     return 0;
   });
 }

@@ -120,4 +120,11 @@ template <typename R>
 void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double* uniforms,
                         uint8_t* bits_col, int64_t bit_stride, cx<R>* env_out, cudaStream_t s);
 
+// tcgen05 (kind::tf32, 3xTF32 split) complex64 GEMM: C = A . B, row-major
+// complex; ws must hold tc_workspace_bytes(M, N, K).
+size_t tc_workspace_bytes(int64_t M, int64_t N, int64_t K);
+void tc_gemm_c64(int64_t M, int64_t N, int64_t K, const cx<float>* A, int64_t lda,
+                 const cx<float>* B, int64_t ldb, cx<float>* C, int64_t ldc, void* ws,
+                 cudaStream_t s);
+
 }  // namespace mb

@@ -83,3 +83,21 @@ def svd_truncate(t: np.ndarray, split: int, epsilon: float, chi_max: int,
     u_k = u.reshape(-1)[: rows * r].reshape(rows, r).copy()
     v_k = v.reshape(-1)[: r * cols].reshape(r, cols).copy()
     return TruncatedSVD(u=u_k, s=s[:r].copy(), v=v_k, discarded_weight=disc.value)
+
+
+def device_gemm(a: np.ndarray, b: np.ndarray, dtype: str = "complex64",
+                tensor_cores: bool = True) -> np.ndarray:
+    """C = A @ B on the device (the pair-blob contraction primitive). With
+    dtype complex64 and tensor_cores=True this runs the tcgen05 kind::tf32
+    kernel (3xTF32 split); otherwise the CUDA-core tile kernel."""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    b = np.ascontiguousarray(b, dtype=np.complex128)
+    m, k = a.shape
+    k2, n = b.shape
+    if k != k2:
+        raise ValueError("inner dimensions differ")
+    c = np.empty((m, n), dtype=np.complex128)
+    lib = nat.load()
+    nat.check(lib.mb_gemm(nat.dptr(a), nat.dptr(b), m, n, k, nat.DTYPES[dtype],
+                          int(bool(tensor_cores)), nat.dptr(c)), "mb_gemm")
+    return c

@@ -110,6 +110,23 @@ def test_svd_large_path(shape):
         assert np.abs(rec - rec_ref).max() < 1e-10
 
 
+@pytest.mark.parametrize("shape", [(128, 64, 32), (130, 70, 45), (512, 384, 256), (1024, 1024, 96)])
+def test_tcgen05_complex_gemm(shape):
+    """tcgen05 kind::tf32 GEMM (3xTF32) against numpy and the CUDA-core tiles."""
+    m, n, k = shape
+    rng = np.random.default_rng(m + n + k)
+    a = rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k))
+    b = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+    ref = a @ b
+    tc = pb.tensor.device_gemm(a, b, "complex64", tensor_cores=True)
+    cc = pb.tensor.device_gemm(a, b, "complex64", tensor_cores=False)
+    d64 = pb.tensor.device_gemm(a, b, "complex128", tensor_cores=False)
+    scale = np.sqrt(k) * 2
+    assert np.abs(d64 - ref).max() <= 1e-12 * scale
+    assert np.abs(cc - ref).max() <= 5e-6 * scale
+    assert np.abs(tc - ref).max() <= 5e-6 * scale, np.abs(tc - ref).max()
+
+
 # ---- chain operations vs the oracle -------------------------------------------------
 
 @pytest.mark.parametrize("side", ["left", "right"])
