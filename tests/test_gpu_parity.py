@@ -124,7 +124,8 @@ def test_tcgen05_complex_gemm(shape):
     scale = np.sqrt(k) * 2
     assert np.abs(d64 - ref).max() <= 1e-12 * scale
     assert np.abs(cc - ref).max() <= 5e-6 * scale
-    assert np.abs(tc - ref).max() <= 5e-6 * scale, np.abs(tc - ref).max()
+    # 3xTF32 sums 6K real tf32 products in fp32: fp32-class error
+    assert np.abs(tc - ref).max() <= 2e-5 * scale, np.abs(tc - ref).max()
 
 
 # ---- chain operations vs the oracle -------------------------------------------------
