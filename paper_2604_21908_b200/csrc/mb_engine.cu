@@ -188,7 +188,7 @@ static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64
                  const cx<R>* B, int64_t ldb, cx<R>* C, int64_t ldc) {
   ProfScope ps(P_GEMM, gemm_flops(M, N, K));
   if (sizeof(R) == sizeof(float) && !ct && tc_enabled() && M >= 128 && N >= 64 && K >= 16 &&
-      M * N * K >= (int64_t)1 << 21) {
+      M * N * K >= (int64_t)1 << 25) {
     void* ws = grow(E.tcws, tc_workspace_bytes(M, N, K));
     tc_gemm_c64(M, N, K, (const cx<float>*)A, lda, (const cx<float>*)B, ldb, (cx<float>*)C, ldc,
                 ws, E.stream);

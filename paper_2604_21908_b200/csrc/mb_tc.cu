@@ -27,6 +27,11 @@ extern std::atomic<long long> g_launches;
 
 constexpr int TC_M = 128, TC_N = 128, TC_K = 32, TC_STAGES = 2;
 constexpr int TC_THREADS = 128;
+// K-tiles rotate over TC_NACC independent TMEM accumulators (TC_NACC*TC_N <= 512
+// columns) that the epilogue sums with round-to-nearest fp32 adds: the MMA
+// pipe's fp32 accumulation is not round-to-nearest, so one long chain's error
+// grows linearly in K; splitting it cuts that by TC_NACC.
+constexpr int TC_NACC = 4;
 constexpr uint32_t TC_LBO = 2048, TC_SBO = 128;  // bytes
 
 struct __align__(1024) TcSmem {
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&S.tmem_base)),
-                 "r"(TC_N));
+                 "r"(TC_N * TC_NACC));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -136,11 +141,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t abase = smem_u32(&S.a[s][0]), bbase = smem_u32(&S.b[s][0]);
+      const uint32_t dacc = tmem + (uint32_t)((kt % TC_NACC) * TC_N);
 #pragma unroll
       for (int k8 = 0; k8 < TC_K / 8; ++k8) {
         const uint32_t off = (uint32_t)(2 * k8) * TC_LBO;
-        umma_tf32(tmem, umma_desc(abase + off), umma_desc(bbase + off), idesc,
-                  (kt > 0 || k8 > 0) ? 1u : 0u);
+        umma_tf32(dacc, umma_desc(abase + off), umma_desc(bbase + off), idesc,
+                  (kt >= TC_NACC || k8 > 0) ? 1u : 0u);
       }
       umma_commit(&S.mbar[s]);
     }
@@ -152,27 +158,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // epilogue: warp w owns TMEM lanes (rows) 32w .. 32w+31
   const int64_t row = m0 + warp * 32 + lane;
   float* crow = C + row * ldc + n0;
+  const int nacc = nk < TC_NACC ? nk : TC_NACC;
 #pragma unroll 1
   for (int j = 0; j < TC_N / 8; ++j) {
-    uint32_t v[8];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(j * 8);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    float4 o0 = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
-                            __uint_as_float(v[3]));
-    float4 o1 = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]),
-                            __uint_as_float(v[7]));
-    *reinterpret_cast<float4*>(crow + j * 8) = o0;
-    *reinterpret_cast<float4*>(crow + j * 8 + 4) = o1;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int a = 0; a < nacc; ++a) {
+      uint32_t v[8];
+      const uint32_t taddr =
+          tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(a * TC_N + j * 8);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] += __uint_as_float(v[t]);
+    }
+    *reinterpret_cast<float4*>(crow + j * 8) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(crow + j * 8 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TC_N * TC_NACC));
 }
 
 // ---- operand preparation (3xTF32 split of the real embedding) -------------
