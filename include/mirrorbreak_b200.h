@@ -98,6 +98,14 @@ int mb_pair_swap(mb_chain* c, int bond, int swap_top, int swap_bottom, double ep
  * decompositions batched on the device.                        unswap.py:104-112 */
 int mb_swap_extents(mb_chain* c, int bond, int nsides, const int* sides, double eps,
                     int64_t chi_max, int64_t* extents);
+/* Batched candidate scoring for one (side, parity) batch of disjoint bonds
+ * (unswap.py:214-240 / paper App. A.1): for each bond with mine[t] != 0 the
+ * center is moved onto it and the truncated ranks of the blob (baseline) and
+ * of the swapped blob (extent) are computed — all values-only decompositions
+ * of the batch in one batched launch, one read-back. Bonds of other shards
+ * report -1 (merged across ranks by an all-reduce(MAX) on the host). */
+int mb_batch_swap_extents(mb_chain* c, int nb, const int* bonds, const int* mine, int side,
+                          double eps, int64_t chi_max, int64_t* baselines, int64_t* extents);
 /* Two-sided sweep: orthogonalize left->right, truncate right->left,
  * renormalize into log_norm; center ends at 0.                 chains.py:262-285 */
 int mb_compress(mb_chain* c, double eps, int64_t chi_max);

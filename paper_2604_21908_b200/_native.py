@@ -58,6 +58,7 @@ _SIGS = {
     "mb_move_center": (_i, [_p, _i]),
     "mb_pair_swap": (_i, [_p, _i, _i, _i, _d, _i64, _i]),
     "mb_swap_extents": (_i, [_p, _i, _i, _ip, _d, _i64, _i64p]),
+    "mb_batch_swap_extents": (_i, [_p, _i, _ip, _ip, _i, _d, _i64, _i64p, _i64p]),
     "mb_compress": (_i, [_p, _d, _i64]),
     "mb_frobenius_norm": (_i, [_p, _dp]),
     "mb_apply_to_zero": (_p, [_p, _d, _i64]),

@@ -560,6 +560,82 @@ static void swap_extents(mb_chain& c, int b, int ns, const int* sides, double ep
   for (int k = 0; k < ns; ++k) out[k] = E.h_info[3 * k];
 }
 
+// Batched candidate scoring for one (side, parity) batch of disjoint bonds
+// (unswap.py:214-240, App. A.1). For every bond flagged in `mine`, with the
+// center moved onto it: baseline = truncated rank of the blob, extent =
+// truncated rank of the swapped blob — all values-only decompositions of the
+// batch go out together and are read back with one sync. Unflagged bonds
+// (another rank's shard) report -1.
+template <typename R>
+static void batch_extents(mb_chain& c, int nb, const int* bonds, const int* mine, int side,
+                          double eps, int64_t chi, int64_t* base_out, int64_t* ext_out) {
+  require(c.d == 4, "swap scoring on a non-operator chain");
+  require(side >= 0 && side <= 2, "bad side");
+  std::vector<Buf> keep;
+  std::vector<SvdJob<R>> jobs;
+  std::vector<int> owner;  // job -> 2*t (+1 for the candidate)
+  Gate4<R> sw = swap_gate<R>();
+  int njobs = 0;
+  for (int t = 0; t < nb; ++t) njobs += mine[t] ? 2 : 0;
+  Buf dinfo = alloc(sizeof(int64_t) * 3 * (size_t)(njobs > 0 ? njobs : 1));
+  Buf ddisc = alloc(sizeof(double) * (size_t)(njobs > 0 ? njobs : 1));
+  for (int t = 0; t < nb; ++t) {
+    base_out[t] = ext_out[t] = -1;
+    if (!mine[t]) continue;
+    const int b = bonds[t];
+    require(b >= 0 && b + 1 < c.n, "bond out of range");
+    move_center<R>(c, b);
+    Site A = c.s[b], B = c.s[b + 1];
+    const int64_t l = A.l, r = B.r, M = 4 * l, N = 4 * r, K = A.r;
+    const int64_t p = M < N ? M : N, q = M < N ? N : M;
+    for (int v = 0; v < 2; ++v) {
+      Buf th = alloc((size_t)(M * N) * sizeof(cx<R>));
+      keep.push_back(th);
+      gemm<R>(false, M, N, K, P<R>(A), K, P<R>(B), N, (cx<R>*)th->p, N);
+      if (v == 1) {
+        ProfScope ps(P_GATE, 0.0);
+        if (side == MB_SIDE_LEFT || side == MB_SIDE_BOTH)
+          launch_gate2<R>((cx<R>*)th->p, sw, l, r, true, E.stream);
+        if (side == MB_SIDE_RIGHT || side == MB_SIDE_BOTH)
+          launch_gate2<R>((cx<R>*)th->p, sw, l, r, false, E.stream);
+      }
+      Buf bx = alloc((size_t)(p * q) * sizeof(cx<R>));
+      Buf bs = alloc((size_t)(2 * p) * sizeof(R));
+      Buf bp = alloc((size_t)p * sizeof(int));
+      keep.push_back(bx);
+      keep.push_back(bs);
+      keep.push_back(bp);
+      SvdJob<R> j;
+      j.A = (cx<R>*)th->p;
+      j.X = (cx<R>*)bx->p;
+      j.V = nullptr;
+      j.sig = (R*)bs->p;
+      j.perm = (int*)bp->p;
+      j.m = M;
+      j.n = N;
+      j.eps = eps;
+      j.chi = chi;
+      j.info = (int64_t*)dinfo->p + 3 * jobs.size();
+      j.disc = (double*)ddisc->p + jobs.size();
+      j.W = nullptr;
+      jobs.push_back(j);
+      owner.push_back(2 * t + v);
+    }
+  }
+  // every rank ends the pass with the center on the batch's last bond, so the
+  // replicas of all ranks stay bit-identical (center moves compose exactly)
+  move_center<R>(c, bonds[nb - 1]);
+  if (jobs.empty()) return;
+  run_jobs<R>(jobs.data(), (int)jobs.size());
+  std::vector<int64_t> info(3 * jobs.size());
+  d2h(info.data(), dinfo->p, sizeof(int64_t) * info.size());
+  sync();
+  for (size_t k = 0; k < jobs.size(); ++k) {
+    const int t = owner[k] / 2;
+    (owner[k] % 2 ? ext_out : base_out)[t] = info[3 * k];
+  }
+}
+
 // Right-to-left truncation step at site i (chains.py:273-280, 310-315).
 template <typename R>
 static void truncate_left(mb_chain& c, int i, double eps, int64_t chi) {
@@ -1036,6 +1112,16 @@ int mb_swap_extents(mb_chain* c, int bond, int ns, const int* sides, double eps,
   MB_TRY({
     if (c->dtype == MB_C64) swap_extents<float>(*c, bond, ns, sides, eps, chi, out);
     else swap_extents<double>(*c, bond, ns, sides, eps, chi, out);
+    return 0;
+  });
+}
+
+int mb_batch_swap_extents(mb_chain* c, int nb, const int* bonds, const int* mine, int side,
+                          double eps, int64_t chi, int64_t* baselines, int64_t* extents) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    if (c->dtype == MB_C64) batch_extents<float>(*c, nb, bonds, mine, side, eps, chi, baselines, extents);
+    else batch_extents<double>(*c, nb, bonds, mine, side, eps, chi, baselines, extents);
     return 0;
   });
 }

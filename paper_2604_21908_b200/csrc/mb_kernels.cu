@@ -1041,7 +1041,7 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
   // converges slower than X itself (c20: 14.4k vs 3.5k sweeps), so the plain
   // path is the default.
   static const int allow_pre = env_int("MB_JACOBI_QR", 0);
-  const int precond = allow_pre && (J.V == nullptr || J.eps >= 1e-6);
+  const int precond = allow_pre && J.W != nullptr && (J.V == nullptr || J.eps >= 1e-6);
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   if (J.A) {
     int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);

@@ -19,6 +19,7 @@ import numpy as np
 from . import _native as nat
 from .chains import MatrixProductOperator, total_elements
 from .routing import QubitPermutation
+from .sharding import Comm, unswap_parity_batched
 
 _EVALUATION_SLACK = 16
 
@@ -38,9 +39,10 @@ class UnswapConfig:
     def __post_init__(self):
         if self.acceptance not in ("strict", "relaxed"):
             raise ValueError(f"acceptance must be strict or relaxed, got {self.acceptance!r}")
-        if self.strategy not in ("sequential", "parity-parallel"):
+        if self.strategy not in ("sequential", "parity-parallel", "parity-batched"):
             raise ValueError(
-                f"strategy must be sequential or parity-parallel, got {self.strategy!r}")
+                "strategy must be sequential, parity-parallel or parity-batched, "
+                f"got {self.strategy!r}")
         if self.max_outer_iterations < 1:
             raise ValueError("max_outer_iterations must be >= 1")
 
@@ -89,6 +91,37 @@ class _Work:
         nat.check(nat._lib.mb_swap_extents(self.m._h, bond, len(sides), codes, self.cfg.epsilon,
                                            self.cfg.chi_max, nat.i64ptr(out)), "swap extents")
         return [int(x) for x in out]
+
+    def score_batch(self, bonds, mine, side):
+        """Device batch scoring of one (side, parity) batch (this rank's shard)."""
+        nb = len(bonds)
+        b_arr = (C.c_int * nb)(*bonds)
+        m_arr = (C.c_int * nb)(*mine)
+        base = np.full(nb, -1, dtype=np.int64)
+        ext = np.full(nb, -1, dtype=np.int64)
+        nat.check(nat._lib.mb_batch_swap_extents(self.m._h, nb, b_arr, m_arr, nat.SIDE[side],
+                                                 self.cfg.epsilon, self.cfg.chi_max,
+                                                 nat.i64ptr(base), nat.i64ptr(ext)),
+                  "batch swap extents")
+        self.refresh()
+        return base, ext
+
+    def accept_recenter(self, bond: int, side: str) -> None:
+        """Apply a batch-accepted swap with the center moved onto the bond."""
+        nat.check(nat._lib.mb_pair_swap(self.m._h, bond, int(side in ("left", "both")),
+                                        int(side in ("right", "both")), self.cfg.epsilon,
+                                        self.cfg.chi_max, 1), "apply batched candidate")
+        self._record(bond, side)
+
+    def _record(self, bond: int, side: str) -> None:
+        self.refresh()
+        tau = QubitPermutation.transposition(self.n, bond, bond + 1)
+        if side in ("left", "both"):
+            self.left = self.left.compose(tau)
+        if side in ("right", "both"):
+            self.right = tau.compose(self.right)
+        self.accepted += 1
+        self.log.append((bond, side))
 
     def accept(self, bond: int, side: str) -> None:
         """Materialize the candidate and record the swap (unswap.py:84-92, 115-121)."""
@@ -177,7 +210,22 @@ def unswap_parallel(m: MatrixProductOperator, cfg: UnswapConfig) -> UnswapResult
     return _result(w, before)
 
 
-def unswap(m: MatrixProductOperator, cfg: UnswapConfig) -> UnswapResult:
+def unswap_batched(m: MatrixProductOperator, cfg: UnswapConfig,
+                   comm: Comm | None = None) -> UnswapResult:
+    """Parity batches scored in one batched device pass each, optionally
+    sharded over the ranks of ``comm`` (sharding.py). Not bit-identical to the
+    reference's bond-by-bond re-truncation order, which ``parity-parallel``
+    keeps; see DESIGN.md."""
+    w = _Work(m, cfg)
+    before = total_elements(m)
+    unswap_parity_batched(w, cfg.acceptance == "relaxed", cfg.max_outer_iterations,
+                          comm or Comm())
+    return _result(w, before)
+
+
+def unswap(m: MatrixProductOperator, cfg: UnswapConfig, comm: Comm | None = None) -> UnswapResult:
     if cfg.strategy == "sequential":
         return unswap_sequential(m, cfg)
+    if cfg.strategy == "parity-batched":
+        return unswap_batched(m, cfg, comm)
     return unswap_parallel(m, cfg)
