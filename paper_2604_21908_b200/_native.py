@@ -8,6 +8,7 @@ or no CUDA device is usable, every chain operation raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
@@ -89,7 +90,9 @@ def load(init: bool = True):
             fn.argtypes = args
         _lib = lib
     if init and not _ready:
-        rc = _lib.mb_init(0)
+        # one process per GPU: bind the rank's local device
+        dev = int(os.environ.get("MB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        rc = _lib.mb_init(dev)
         if rc != 0:
             raise NativeError(f"mb_init failed: {_lib.mb_last_error().decode()}")
         _ready = True
