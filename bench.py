@@ -92,11 +92,13 @@ class Clocks:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
                 try:
+                    dev = os.environ.get("MB_DEVICE", os.environ.get("LOCAL_RANK", "0"))
                     out = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-i", os.environ.get("LOCAL_RANK", "0")],
+                                          "-i", dev],
                                          capture_output=True, text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    row = [x.strip() for x in out.split(",")] if out else []
+                    if len(row) >= 7:
+                        self.rows.append(row)
                 except Exception:
                     pass
                 self._stop.wait(0.2)
