@@ -332,8 +332,13 @@ __device__ double pair_trace(PairSmem<R, W2>& S) {
 }
 
 // Two-sided cyclic Jacobi on the Hermitian h; accumulates the rotation in w.
+// Only the leading np (even) slots take part (the rest are zero padding).
+// Each round computes the rotations of its np/2 disjoint pairs, then updates
+// every 2x2 block of h in ONE phase, h[{ja,ka},{jb,kb}] <- J_a^H h J_b, and
+// w[:, {jb,kb}] <- w J_b (two barriers per round instead of three).
 template <typename R, int W2>
-__device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int max_sweeps) {
+__device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int max_sweeps,
+                         int np = W2) {
   const int tid = threadIdx.x;
   for (int e = tid; e < W2 * W2; e += blockDim.x) {
     int a = e / W2, b = e % W2;
@@ -341,13 +346,14 @@ __device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int m
   }
   __syncthreads();
   const double t2 = tol * tol, f2 = floor_abs * floor_abs;
+  const int npairs = np / 2;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) S.flag = 0;
     __syncthreads();
-    for (int rnd = 0; rnd < W2 - 1; ++rnd) {
-      if (tid < W2 / 2) {
+    for (int rnd = 0; rnd < np - 1; ++rnd) {
+      if (tid < npairs) {
         int j, k;
-        tournament(W2, rnd, tid, j, k);
+        tournament(np, rnd, tid, j, k);
         if (j > k) { int t = j; j = k; k = t; }
         S.pj[tid] = j;
         S.pk[tid] = k;
@@ -370,33 +376,39 @@ __device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int m
         }
       }
       __syncthreads();
-      // rows: H <- J^H H
-      for (int e = tid; e < (W2 / 2) * W2; e += blockDim.x) {
-        int p = e / W2, c = e % W2;
-        R cc = S.cs[p], ss = S.sn[p];
-        if (ss == 0) continue;
-        int j = S.pj[p], k = S.pk[p];
-        cx<R> ep = cconj(S.ph[p]);
-        cx<R> hj = S.h[j][c], hk = S.h[k][c];
-        cx<R> ek = cmul(ep, hk);
-        S.h[j][c] = csub(cscale(hj, cc), cscale(ek, ss));
-        S.h[k][c] = cadd(cscale(hj, ss), cscale(ek, cc));
-      }
-      __syncthreads();
-      // columns: H <- H J, W <- W J
-      for (int e = tid; e < (W2 / 2) * W2 * 2; e += blockDim.x) {
-        int which = e / ((W2 / 2) * W2);
-        int e2 = e % ((W2 / 2) * W2);
-        int p = e2 / W2, rr = e2 % W2;
-        R cc = S.cs[p], ss = S.sn[p];
-        if (ss == 0) continue;
-        int j = S.pj[p], k = S.pk[p];
-        cx<R> ep = S.ph[p];
-        cx<R>(*M)[W2 + 1] = which ? S.w : S.h;
-        cx<R> mj = M[rr][j], mk_ = M[rr][k];
-        cx<R> ek = cmul(mk_, ep);
-        M[rr][j] = csub(cscale(mj, cc), cscale(ek, ss));
-        M[rr][k] = cadd(cscale(mj, ss), cscale(ek, cc));
+      // h blocks: npairs x npairs 2x2 blocks
+      const int nblk = npairs * npairs;
+      for (int e = tid; e < nblk + np * npairs; e += blockDim.x) {
+        if (e < nblk) {
+          const int pa = e / npairs, pb = e % npairs;
+          const R ca = S.cs[pa], sa = S.sn[pa], cb = S.cs[pb], sb = S.sn[pb];
+          if (sa == 0 && sb == 0) continue;
+          const int ja = S.pj[pa], ka = S.pk[pa], jb = S.pj[pb], kb = S.pk[pb];
+          const cx<R> ea = S.ph[pa], eb = S.ph[pb];
+          const cx<R> eac = cconj(ea);
+          cx<R> b00 = S.h[ja][jb], b01 = S.h[ja][kb], b10 = S.h[ka][jb], b11 = S.h[ka][kb];
+          // T = J_a^H B : rows (j,k)
+          cx<R> e10 = cmul(eac, b10), e11 = cmul(eac, b11);
+          cx<R> t00 = csub(cscale(b00, ca), cscale(e10, sa));
+          cx<R> t01 = csub(cscale(b01, ca), cscale(e11, sa));
+          cx<R> t10 = cadd(cscale(b00, sa), cscale(e10, ca));
+          cx<R> t11 = cadd(cscale(b01, sa), cscale(e11, ca));
+          // B' = T J_b : cols (j,k)
+          cx<R> f01 = cmul(t01, eb), f11 = cmul(t11, eb);
+          S.h[ja][jb] = csub(cscale(t00, cb), cscale(f01, sb));
+          S.h[ja][kb] = cadd(cscale(t00, sb), cscale(f01, cb));
+          S.h[ka][jb] = csub(cscale(t10, cb), cscale(f11, sb));
+          S.h[ka][kb] = cadd(cscale(t10, sb), cscale(f11, cb));
+        } else {
+          const int f = e - nblk, rr = f / npairs, pb = f % npairs;
+          const R cb = S.cs[pb], sb = S.sn[pb];
+          if (sb == 0) continue;
+          const int jb = S.pj[pb], kb = S.pk[pb];
+          const cx<R> eb = S.ph[pb];
+          cx<R> mj = S.w[rr][jb], mk_ = cmul(S.w[rr][kb], eb);
+          S.w[rr][jb] = csub(cscale(mj, cb), cscale(mk_, sb));
+          S.w[rr][kb] = cadd(cscale(mj, sb), cscale(mk_, cb));
+        }
       }
       __syncthreads();
     }
@@ -508,7 +520,7 @@ __global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
     pair_gram<R, W2>(S, J.X, q);
     const double fl = abs_floor<R>(q) * sqrt(pair_trace<R, W2>(S));
     if (!pair_offdiag<R, W2>(S, tol, fl)) { converged = 1; break; }
-    pair_evd<R, W2>(S, tol, fl, 30);
+    pair_evd<R, W2>(S, tol, fl, 30, (int)(p + (p & 1)));
     pair_apply<R, W2>(S, J.X, q);
     if (J.V) pair_apply<R, W2>(S, J.V, p);
   }
