@@ -11,6 +11,7 @@
 // gauge-invariant).
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -194,7 +195,24 @@ static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64
                 ws, E.stream);
     return;
   }
+  static FILE* log = getenv("MB_GEMM_LOG") ? fopen(getenv("MB_GEMM_LOG"), "w") : nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (log) {  // debug: shapes and device time of the CUDA-core GEMMs
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, E.stream);
+  }
   launch_gemm<R>(ct, M, N, K, A, lda, B, ldb, C, ldc, E.stream);
+  if (log) {
+    cudaEventRecord(t1, E.stream);
+    cudaEventSynchronize(t1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    fprintf(log, "%d %lld %lld %lld %.1f\n", (int)ct, (long long)M, (long long)N, (long long)K,
+            ms * 1000.0);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
 }
 
 // ---- SVD orchestration ---------------------------------------------------
@@ -222,6 +240,10 @@ static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double
 }
 
 template <typename R>
+static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n);
+static int g_tag = 0;  // debug (MB_SVD_LOG): which engine operation issued the SVD
+
+template <typename R>
 static void run_jobs(SvdJob<R>* jobs, int nj) {
   std::vector<SvdJob<R>> small;
   int maxp = 0;
@@ -238,9 +260,32 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       double p = (double)(j.m < j.n ? j.m : j.n), q = (double)(j.m < j.n ? j.n : j.m);
       fl += 2.0 * 8.0 * p * p * q;  // one Gram + one rotation pass (lower bound)
     }
-    ProfScope ps(P_SVD_SMALL, fl);
-    launch_svd_small<R>(small.data(), (int)small.size(), maxp, E.stream);
+    static FILE* log = getenv("MB_SVD_LOG") ? fopen(getenv("MB_SVD_LOG"), "w") : nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (log) {
+      cudaEventCreate(&t0);
+      cudaEventCreate(&t1);
+      cudaEventRecord(t0, E.stream);
+    }
+    {
+      ProfScope ps(P_SVD_SMALL, fl);
+      launch_svd_small<R>(small.data(), (int)small.size(), maxp, E.stream);
+    }
     E.counters[0] += (long long)small.size();
+    if (log) {  // debug: per-launch shapes, Jacobi iterations and device time
+      cudaEventRecord(t1, E.stream);
+      cudaEventSynchronize(t1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t0, t1);
+      for (auto& j : small) {
+        int64_t info[3];
+        cudaMemcpy(info, j.info, sizeof(info), cudaMemcpyDeviceToHost);
+        fprintf(log, "%d %lld %lld %lld %lld %.1f\n", (int)sizeof(R) * 100 + g_tag, (long long)j.m,
+                (long long)j.n, (long long)info[2], (long long)info[0], ms * 1000.0 / small.size());
+      }
+      cudaEventDestroy(t0);
+      cudaEventDestroy(t1);
+    }
   }
   for (int i = 0; i < nj; ++i) {
     int64_t p = jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n;
@@ -248,7 +293,17 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
       ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * (double)p * (double)p * q);
       double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
+      static FILE* llog = getenv("MB_SVD_LOG") ? fopen((std::string(getenv("MB_SVD_LOG")) + ".large").c_str(), "w") : nullptr;
+      auto w0 = std::chrono::steady_clock::now();
       svd_large<R>(jobs[i], reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, E.stream);
+      if (llog) {  // debug: shapes, sweeps and host wall time of the large path
+        cudaStreamSynchronize(E.stream);
+        double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
+        int64_t info[3];
+        cudaMemcpy(info, jobs[i].info, sizeof(info), cudaMemcpyDeviceToHost);
+        fprintf(llog, "%d %lld %lld %lld %lld %.1f\n", g_tag, (long long)jobs[i].m,
+                (long long)jobs[i].n, (long long)info[2], (long long)info[0], us);
+      }
       E.counters[1]++;
       E.counters[3]++;
     }
@@ -371,6 +426,7 @@ static void push_right(mb_chain& c, int i) {
     nB = new_site<R>(n, d, B.r);
     gemm<R>(false, n, rn, n, Rm, n, P<R>(B), rn, P<R>(nB), rn);
   } else {
+    g_tag = 1;
     SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
     run_jobs<R>(&j, 1);
     nA = new_site<R>(A.l, d, n);
@@ -407,6 +463,7 @@ static void push_left(mb_chain& c, int i) {
     nP = new_site<R>(Pv.l, d, m);
     gemm<R>(false, pm, m, m, P<R>(Pv), m, L, m, P<R>(nP), m);
   } else {
+    g_tag = 2;
     SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
     run_jobs<R>(&j, 1);
     nA = new_site<R>(m, d, A.r);
@@ -460,6 +517,7 @@ static cx<R>* blob(mb_chain& c, int b, int slot, int64_t& l, int64_t& r) {
 // Truncated re-split of theta into sites (b, b+1), S on the right (chains.py:157-167).
 template <typename R>
 static void resplit(mb_chain& c, int b, cx<R>* th, int64_t l, int64_t r, double eps, int64_t chi) {
+  g_tag = 3;
   SvdJob<R> j = make_job<R>(0, th, 4 * l, 4 * r, eps, chi, true);
   run_jobs<R>(&j, 1);
   read_info(1);
@@ -553,6 +611,7 @@ static void swap_extents(mb_chain& c, int b, int ns, const int* sides, double ep
     ProfScope ps(P_GATE, 0.0);
     if (sd == MB_SIDE_LEFT || sd == MB_SIDE_BOTH) launch_gate2<R>(th, sw, l, r, true, E.stream);
     if (sd == MB_SIDE_RIGHT || sd == MB_SIDE_BOTH) launch_gate2<R>(th, sw, l, r, false, E.stream);
+    g_tag = 4;
     jobs[k] = make_job<R>(k, th, M, N, eps, chi, false);
   }
   run_jobs<R>(jobs, ns);
@@ -642,6 +701,7 @@ static void truncate_left(mb_chain& c, int i, double eps, int64_t chi) {
   const int d = c.d;
   Site A = c.s[i], Pv = c.s[i - 1];
   const int64_t m = A.l, n = (int64_t)d * A.r;
+  g_tag = 5;
   SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, eps, chi, true);
   run_jobs<R>(&j, 1);
   read_info(1);
@@ -873,6 +933,7 @@ static void svd_host(const double* a, int64_t m, int64_t n, double eps, int64_t 
                      double* s, double* v, int64_t* rank, double* disc) {
   Buf dA = alloc((size_t)(m * n) * sizeof(cx<R>));
   upload<R>(a, (cx<R>*)dA->p, m * n);
+  g_tag = 6;
   SvdJob<R> j = make_job<R>(0, (cx<R>*)dA->p, m, n, eps, chi, true);
   run_jobs<R>(&j, 1);
   read_info(1);

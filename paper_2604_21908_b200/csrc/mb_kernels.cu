@@ -278,6 +278,7 @@ __device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64
       S.xs[c][t] = (gc >= 0 && i0 + t < r1) ? X[(int64_t)gc * q + i0 + t] : mk<R>(0, 0);
     }
     __syncthreads();
+    if (tid < 256) {  // 16 x 16 thread tile; extra threads only stage rows
 #pragma unroll 4
     for (int t = 0; t < TQ; ++t) {
       cx<R> a[TM], b[TM];
@@ -290,12 +291,14 @@ __device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64
 #pragma unroll
         for (int j = 0; j < TM; ++j) cfmac(acc[i][j], a[i], b[j]);
     }
+    }
     __syncthreads();
   }
+  if (tid < 256)
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TM; ++j) S.h[ty + 16 * i][tx + 16 * j] = acc[i][j];
+      for (int j = 0; j < TM; ++j) S.h[ty + 16 * i][tx + 16 * j] = acc[i][j];
   __syncthreads();
 }
 
@@ -337,8 +340,8 @@ __device__ double pair_trace(PairSmem<R, W2>& S) {
 // every 2x2 block of h in ONE phase, h[{ja,ka},{jb,kb}] <- J_a^H h J_b, and
 // w[:, {jb,kb}] <- w J_b (two barriers per round instead of three).
 template <typename R, int W2>
-__device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int max_sweeps,
-                         int np = W2) {
+__device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int max_sweeps,
+                        int np = W2) {
   const int tid = threadIdx.x;
   for (int e = tid; e < W2 * W2; e += blockDim.x) {
     int a = e / W2, b = e % W2;
@@ -412,9 +415,10 @@ __device__ void pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int m
       }
       __syncthreads();
     }
-    if (S.flag == 0) break;
+    if (S.flag == 0) return sweep + 1;
     __syncthreads();
   }
+  return max_sweeps;
 }
 
 // Y[:, cols] <- Y[:, cols] W for a column-major matrix with column length len.
@@ -498,13 +502,20 @@ __device__ void job_init(const SvdJob<R>& J, int64_t p, int64_t q) {
   __syncthreads();
 }
 
+// Inner EVD sweep cap of the small path. Quadratic convergence finishes the
+// resolvable part of the Gram in a few sweeps; past that, rotations among
+// directions at the Gram's rounding level only churn (seen on contraction
+// blobs: 30-sweep runs). The outer loop recomputes a fresh Gram of the rotated
+// columns, which resolves what is left.
+constexpr int kSmallEvdSweeps = 6;
+
 template <typename R>
 struct JobPack {
   SvdJob<R> j[kPackJobs];
 };
 
-template <typename R, int W2>
-__global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
+template <typename R, int W2, int NT>
+__global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
   const SvdJob<R> J = pack.j[blockIdx.x];
@@ -520,7 +531,7 @@ __global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
     pair_gram<R, W2>(S, J.X, q);
     const double fl = abs_floor<R>(q) * sqrt(pair_trace<R, W2>(S));
     if (!pair_offdiag<R, W2>(S, tol, fl)) { converged = 1; break; }
-    pair_evd<R, W2>(S, tol, fl, 30, (int)(p + (p & 1)));
+    pair_evd<R, W2>(S, tol, fl, kSmallEvdSweeps, (int)(p + (p & 1)));
     pair_apply<R, W2>(S, J.X, q);
     if (J.V) pair_apply<R, W2>(S, J.V, p);
   }
@@ -555,27 +566,143 @@ __global__ void __launch_bounds__(256) k_svd_small(const JobPack<R> pack) {
   }
 }
 
+// Small-p SVD for tall problems: the CL CTAs of a cluster split the q rows of
+// one job. Per iteration: partial Grams -> DSMEM reduction into rank 0 ->
+// convergence test + EVD on rank 0 -> rotation broadcast over DSMEM -> every
+// CTA rotates its rows of X (and V). All iterations, the sort and the rank
+// rule run inside the one launch.
+template <typename R, int W2, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
+    k_svd_small_cl(const JobPack<R> pack) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const SvdJob<R> J = pack.j[blockIdx.x / CL];
+  const int64_t p = J.m < J.n ? J.m : J.n;
+  const int64_t q = J.m < J.n ? J.n : J.m;
+  const int64_t qs = cdiv_d(q, CL), q0 = rank * qs, q1 = q0 + qs < q ? q0 + qs : q;
+  const int64_t ps = cdiv_d(p, CL), p0 = rank * ps, p1 = p0 + ps < p ? p0 + ps : p;
+  // distributed init: this CTA's rows of X and of V
+  for (int64_t j = 0; j < p; ++j)
+    for (int64_t i = q0 + threadIdx.x; i < q1; i += blockDim.x)
+      J.X[j * q + i] = (J.m >= J.n) ? J.A[i * J.n + j] : cconj(J.A[j * J.n + i]);
+  if (J.V)
+    for (int64_t j = 0; j < p; ++j)
+      for (int64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x)
+        J.V[j * p + i] = mk<R>(i == j ? 1 : 0, 0);
+  for (int c = threadIdx.x; c < W2; c += blockDim.x) S.col[c] = c < p ? c : -1;
+  PairSmem<R, W2>* S0 = cluster.map_shared_rank(&S, 0);
+  const double tol = rel_tol<R>(q);
+  int it = 0, converged = 0;
+  for (;; ++it) {
+    cluster.sync();  // every CTA's rows of X are final before the Gram
+    pair_gram<R, W2>(S, J.X, q, q0, q1);
+    cluster.sync();
+    for (int e = threadIdx.x * CL + rank; e < W2 * W2; e += blockDim.x * CL) {
+      const int i = e / W2, j = e % W2;
+      cx<R> acc = mk<R>(0, 0);
+#pragma unroll
+      for (int r = 0; r < CL; ++r) acc = cadd(acc, cluster.map_shared_rank(&S, r)->h[i][j]);
+      S0->h[i][j] = acc;
+    }
+    cluster.sync();
+    if (rank == 0) {
+      const double fl = abs_floor<R>(q) * sqrt(pair_trace<R, W2>(S));
+      const bool rot = it < 16 && pair_offdiag<R, W2>(S, tol, fl);
+      if (rot) pair_evd<R, W2>(S, tol, fl, kSmallEvdSweeps, (int)(p + (p & 1)));
+      __syncthreads();
+      if (threadIdx.x == 0) S.flag = rot ? 1 : 0;
+    }
+    cluster.sync();
+    if (!S0->flag) {
+      converged = it < 16;
+      break;
+    }
+    if (rank != 0)
+      for (int e = threadIdx.x; e < W2 * W2; e += blockDim.x) S.w[e / W2][e % W2] = S0->w[e / W2][e % W2];
+    cluster.sync();
+    pair_apply<R, W2>(S, J.X, q, q0, q1);
+    if (J.V && p0 < p1) pair_apply<R, W2>(S, J.V, p, p0, p1);
+  }
+  if (rank == 0) {
+    __shared__ R sg[W2];
+    for (int c = threadIdx.x; c < W2; c += blockDim.x) {
+      R d = c < p ? S.h[c][c].x : (R)0;
+      sg[c] = d > 0 ? sqrt(d) : (R)0;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += blockDim.x) {
+      R v = sg[c];
+      int pos = 0;
+      for (int c2 = 0; c2 < p; ++c2) {
+        R u = sg[c2];
+        pos += (u > v) || (u == v && c2 < c);
+      }
+      J.sig[pos] = v;
+      J.perm[pos] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      rank_rule<R>(J.sig, (int)p, J.eps, J.chi, &J.info[0], J.disc);
+      J.info[1] = converged ? 0 : 1;
+      J.info[2] = it;
+    }
+  }
+  cluster.sync();  // rank 0's shared memory stays alive until every reader is done
+}
+
+template <typename R, int W2, int CL>
+static void launch_small_cl(const JobPack<R>& pack, int cnt, cudaStream_t s) {
+  static bool attr = false;
+  size_t sm = sizeof(PairSmem<R, W2>);
+  if (!attr) {
+    cudaFuncSetAttribute(k_svd_small_cl<R, W2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
+    attr = true;
+  }
+  k_svd_small_cl<R, W2, CL><<<cnt * CL, 256, sm, s>>>(pack);
+}
+
 template <typename R>
 void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t s) {
   static bool attr32 = false, attr64 = false;
+  static const int use_cl = getenv("MB_SMALL_CLUSTER") ? atoi(getenv("MB_SMALL_CLUSTER")) : 1;
+  static const int nt64 = getenv("MB_SMALL_THREADS") ? atoi(getenv("MB_SMALL_THREADS")) : 512;
+  int64_t max_q = 0;
+  for (int i = 0; i < njobs; ++i)
+    max_q = std::max<int64_t>(max_q, jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
+  // tall problems spread their Gram/rotation passes over the CTAs of a cluster
+  const int CL = !use_cl ? 1 : (max_q >= 1024 ? 8 : (max_q >= 256 ? 4 : 1));
   for (int b = 0; b < njobs; b += kPackJobs) {
     JobPack<R> pack;
     int cnt = njobs - b < kPackJobs ? njobs - b : kPackJobs;
     for (int i = 0; i < cnt; ++i) pack.j[i] = jobs[b + i];
-    if (max_p <= 32) {
+    if (CL > 1) {
+      if (max_p <= 32) {
+        if (CL == 8) launch_small_cl<R, 32, 8>(pack, cnt, s);
+        else launch_small_cl<R, 32, 4>(pack, cnt, s);
+      } else {
+        if (CL == 8) launch_small_cl<R, 64, 8>(pack, cnt, s);
+        else launch_small_cl<R, 64, 4>(pack, cnt, s);
+      }
+    } else if (max_p <= 32) {
       size_t sm = sizeof(PairSmem<R, 32>);
       if (!attr32) {
-        cudaFuncSetAttribute(k_svd_small<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_svd_small<R, 32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr32 = true;
       }
-      k_svd_small<R, 32><<<cnt, 256, sm, s>>>(pack);
+      k_svd_small<R, 32, 256><<<cnt, 256, sm, s>>>(pack);
     } else {
       size_t sm = sizeof(PairSmem<R, 64>);
       if (!attr64) {
-        cudaFuncSetAttribute(k_svd_small<R, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_svd_small<R, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_svd_small<R, 64, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr64 = true;
       }
-      k_svd_small<R, 64><<<cnt, 256, sm, s>>>(pack);
+      if (nt64 == 512) k_svd_small<R, 64, 512><<<cnt, 512, sm, s>>>(pack);
+      else k_svd_small<R, 64, 256><<<cnt, 256, sm, s>>>(pack);
     }
     MB_LAUNCH_CHECK();
   }
@@ -648,7 +775,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
   const int rank = (int)cluster.block_rank();
   constexpr int w = W2 / 2;
   int a, b;
-  tournament(NB, rnd, blockIdx.x / CL, a, b);
+  const bool check_only = rnd < 0;
+  if (check_only) {  // every block pair a < b at once: linear index -> (a, b)
+    int idx = blockIdx.x / CL;
+    a = 0;
+    while (idx >= nb - 1 - a) {
+      idx -= nb - 1 - a;
+      ++a;
+    }
+    b = a + 1 + idx;
+  } else {
+    tournament(NB, rnd, blockIdx.x / CL, a, b);
+  }
   for (int c = threadIdx.x; c < W2; c += blockDim.x) {
     int blk = c < w ? a : b;
     int64_t gc = (int64_t)blk * w + (c % w);
@@ -676,6 +814,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
     const double tol = rel_tol<R>(q);
     const double fl = abs_floor<R>(q) * sqrt(*fro2);
     bool rot = pair_offdiag<R, W2>(S, tol, fl);
+    if (rot && check_only) {
+      if (threadIdx.x == 0) atomicAdd(flag, 1);
+      rot = false;
+    }
     if (rot) pair_evd<R, W2>(S, tol, fl, inner_sweeps);
     if (threadIdx.x == 0) {
       S.flag = rot ? 1 : 0;
@@ -971,8 +1113,10 @@ static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int
                          (int)sm);
     attr = true;
   }
-  k_jacobi_pair_cl<R, W2, CL><<<(NB / 2) * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev,
-                                                               fro2, inner);
+  // rnd < 0: convergence check of every block pair in one launch
+  const int pairs = rnd < 0 ? nb * (nb - 1) / 2 : NB / 2;
+  k_jacobi_pair_cl<R, W2, CL><<<pairs * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev,
+                                                          fro2, inner);
   MB_LAUNCH_CHECK();
 }
 
@@ -997,22 +1141,35 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, int* fla
   // 8-CTA clusters when the pairs alone cannot fill the chip
   const bool wide = (NB / 2) * 4 < 148 && len >= 8 * 64;
   conv = 0;
-  for (sweeps = 0; sweeps < 60; ++sweeps) {
-    cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
-    for (int rnd = 0; rnd < NB - 1; ++rnd) {
-      if (W2 == 64) {
-        if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
-        else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
-      } else {
-        if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
-        else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
-      }
+  sweeps = 0;
+  auto round = [&](int rnd) {
+    if (W2 == 64) {
+      if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+      else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+    } else {
+      if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+      else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
     }
+  };
+  // Convergence is tested by one all-pairs check launch (block pairs in
+  // parallel, no rotation) before each tournament sweep: inputs that are
+  // already column-orthogonal (frequent in the contraction: canonical-form
+  // moves over flat operator spectra) cost one launch, and the confirming
+  // sweep of the classic loop becomes one launch instead of NB - 1.
+  for (;;) {
+    cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
+    round(-1);
     cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    if (debug) fprintf(stderr, "[svd_large p=%lld len=%lld] sweep %d rotated pairs %d of %d\n",
-                       (long long)p, (long long)len, sweeps, *flag_host, (NB / 2) * (NB - 1));
-    if (*flag_host == 0) { conv = 1; break; }
+    if (debug) fprintf(stderr, "[svd_large p=%lld len=%lld] after %d sweeps: %d of %d pairs open\n",
+                       (long long)p, (long long)len, sweeps, *flag_host, nb * (nb - 1) / 2);
+    if (*flag_host == 0) {
+      conv = 1;
+      break;
+    }
+    if (sweeps == 60) break;
+    for (int rnd = 0; rnd < NB - 1; ++rnd) round(rnd);
+    ++sweeps;
   }
 }
 

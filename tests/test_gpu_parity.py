@@ -110,6 +110,34 @@ def test_svd_large_path(shape):
         assert np.abs(rec - rec_ref).max() < 1e-10
 
 
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+@pytest.mark.parametrize("shape", [(1024, 64), (40, 2048), (300, 20), (64, 256), (1500, 33)])
+def test_svd_small_cluster_path(shape, dtype):
+    """p <= 64 with tall q: the Gram/rotation passes are split over a cluster."""
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    a = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    u, s, v = np.linalg.svd(a, full_matrices=False)
+    s = np.exp(-np.arange(len(s)) / 6.0)
+    s[-len(s) // 4:] = 0.0
+    a = (u * s) @ v
+    s_ref = np.linalg.svd(a, compute_uv=False)
+    tol = 1e-12 if dtype == "complex128" else 2e-6
+    # backward-stable class: absolute error ~ u * sqrt(q) * ||A||_F per value
+    atol = tol * s_ref[0] if dtype == "complex128" else 8 * 6e-8 * np.sqrt(max(shape)) * np.linalg.norm(a)
+    for eps in (0.0, 1e-3):
+        dec = pb.svd_truncate(a, 1, eps, 10**6, dtype=dtype)
+        assert dec.rank == mo.kept_rank(s_ref, eps, 10**6), eps
+        np.testing.assert_allclose(dec.s, s_ref[:dec.rank], rtol=tol, atol=atol)
+        r = dec.rank
+        if eps > 0:  # kept vectors only (eps = 0 keeps the numerical null space)
+            iso = 10 * tol if dtype == "complex128" else 64 * 6e-8 * s_ref[0] / s_ref[r - 1]
+            np.testing.assert_allclose(dec.v @ dec.v.conj().T, np.eye(r), atol=iso)
+            np.testing.assert_allclose(dec.u.conj().T @ dec.u, np.eye(r), atol=iso)
+        else:
+            rec = dec.u @ np.diag(dec.s) @ dec.v
+            assert np.linalg.norm(rec - a) <= 10 * tol * np.linalg.norm(a)
+
+
 @pytest.mark.parametrize("shape", [(128, 64, 32), (130, 70, 45), (512, 384, 256), (1024, 1024, 96)])
 def test_tcgen05_complex_gemm(shape):
     """tcgen05 kind::tf32 GEMM (3xTF32) against numpy and the CUDA-core tiles."""
