@@ -69,6 +69,9 @@ struct Engine {
   static constexpr int kSlots = 4;
   Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots], W[kSlots];
   Buf carry, env[2], amp, misc, tcws;
+  // device-resident sweep runs (k_sweep)
+  Buf sw_X, sw_V, sw_sig, sw_perm, sw_carry, sw_info, sw_disc;
+  int64_t* h_sw_info = nullptr;  // 3 * kSweepMax
   long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [6] h2d bytes, [7] d2h bytes
   // profiling
   bool prof = false;
@@ -478,16 +481,179 @@ static void push_left(mb_chain& c, int i) {
   c.s[i - 1] = nP;
 }
 
+// ---- device-resident sweep runs -------------------------------------------
+//
+// Consecutive small canonical-form steps run inside ONE k_sweep launch (one
+// CTA walks the run; factors go straight into the new sites, the carry into
+// the neighbour, truncation ranks stay on the device). Steps whose
+// factorization or carry product is too big for one SM fall back to the
+// per-step path above. MB_SWEEP=0 disables the runs.
+
+static bool sweep_enabled() {
+  static const bool on = !getenv("MB_SWEEP") || atoi(getenv("MB_SWEEP")) != 0;
+  return on;
+}
+constexpr int64_t kSweepGemmMax = (int64_t)1 << 18;  // complex MACs of a fused carry product
+constexpr int64_t kSweepSvdMax = (int64_t)1 << 20;   // p*p*q of a fused factorization
+
+static bool fuse_svd(int64_t m, int64_t n) {
+  const int64_t p = std::min(m, n), q = std::max(m, n);
+  return p <= kSmallP && p * p * q <= kSweepSvdMax;
+}
+
+template <typename R>
+static bool fuse_right(const mb_chain& c, int i) {
+  const Site &A = c.s[i], &B = c.s[i + 1];
+  const int64_t m = A.l * c.d, n = A.r, rn = (int64_t)c.d * B.r;
+  if (m < n) return m * rn * n <= kSweepGemmMax;
+  if (n > kSmallP && use_qr_steps()) return false;
+  return fuse_svd(m, n) && n * rn * n <= kSweepGemmMax;
+}
+
+template <typename R>
+static bool fuse_left(const mb_chain& c, int i) {
+  const Site &A = c.s[i], &Pv = c.s[i - 1];
+  const int64_t m = A.l, n = (int64_t)c.d * A.r, pm = Pv.l * c.d;
+  if (m > n) return pm * n * m <= kSweepGemmMax;
+  if (m > kSmallP && use_qr_steps()) return false;
+  return fuse_svd(m, n) && pm * m * m <= kSweepGemmMax;
+}
+
+template <typename R>
+static SweepPack<R> sweep_pack(int d) {
+  SweepPack<R> pk;
+  pk.n = 0;
+  pk.d = d;
+  pk.sig = (R*)grow(E.sw_sig, 2 * kSmallP * sizeof(R));
+  pk.perm = (int*)grow(E.sw_perm, kSmallP * sizeof(int));
+  pk.info = (int64_t*)E.sw_info->p;
+  pk.disc = (double*)E.sw_disc->p;
+  pk.tprof = nullptr;
+  return pk;
+}
+
+// size the scratch for the run's largest step and launch it
+template <typename R>
+static void sweep_launch(SweepPack<R>& pk, int64_t max_pq, int64_t max_pp) {
+  pk.X = (cx<R>*)grow(E.sw_X, (size_t)std::max<int64_t>(max_pq, 1) * sizeof(cx<R>));
+  pk.V = (cx<R>*)grow(E.sw_V, (size_t)std::max<int64_t>(max_pp, 1) * sizeof(cx<R>));
+  pk.carry = (cx<R>*)grow(E.sw_carry, (size_t)std::max<int64_t>(max_pq, 1) * sizeof(cx<R>));
+  double fl = 0;
+  for (int t = 0; t < pk.n; ++t) fl += 8.0 * pk.st[t].l * pk.st[t].r;  // nominal
+  static FILE* log = getenv("MB_SVD_LOG") ? fopen((std::string(getenv("MB_SVD_LOG")) + ".sweep").c_str(), "w") : nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (log) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, E.stream);
+    static Buf tp = alloc(sizeof(long long) * 4 * kSweepMax);
+    pk.tprof = (long long*)tp->p;
+  }
+  {
+    ProfScope ps(P_SVD_SMALL, fl);
+    launch_sweep<R>(pk, E.stream);
+  }
+  E.counters[0] += pk.n;
+  if (log) {  // debug: per-run kind, length, largest step and device time
+    cudaEventRecord(t1, E.stream);
+    cudaEventSynchronize(t1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    fprintf(log, "%d %d %lld %lld %.1f\n", pk.st[0].kind, pk.n, (long long)max_pq, (long long)max_pp,
+            ms * 1000.0);
+    if (pk.tprof) {  // per step: l r body emit gemm (cycles)
+      long long h[4 * kSweepMax];
+      cudaMemcpy(h, pk.tprof, sizeof(long long) * 4 * pk.n, cudaMemcpyDeviceToHost);
+      for (int t = 0; t < pk.n; ++t)
+        fprintf(log, "S %d %lld %lld %lld %lld %lld\n", pk.st[t].kind, (long long)pk.st[t].l,
+                (long long)pk.st[t].r, h[4 * t + 1] - h[4 * t], h[4 * t + 2] - h[4 * t + 1],
+                h[4 * t + 3] - h[4 * t + 2]);
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
+}
+
+// push_right for i in [from, to)
+template <typename R>
+static void push_right_range(mb_chain& c, int from, int to) {
+  const int d = c.d;
+  int i = from;
+  while (i < to) {
+    if (!sweep_enabled() || !fuse_right<R>(c, i)) {
+      push_right<R>(c, i);
+      ++i;
+      continue;
+    }
+    SweepPack<R> pk = sweep_pack<R>(d);
+    std::vector<Buf> keep;  // inputs stay allocated until the launch is queued
+    int64_t max_pq = 0, max_pp = 0;
+    while (i < to && pk.n < kSweepMax && fuse_right<R>(c, i)) {
+      Site A = c.s[i], B = c.s[i + 1];
+      const int64_t m = A.l * d, n = A.r, k = std::min(m, n);
+      Site nA = new_site<R>(A.l, d, k), nB = new_site<R>(k, d, B.r);
+      if (m >= n) {
+        max_pq = std::max(max_pq, m * n);
+        max_pp = std::max(max_pp, n * n);
+      }
+      SweepStep<R>& st = pk.st[pk.n++];
+      st = SweepStep<R>{P<R>(A), P<R>(B), P<R>(nA), P<R>(nB), kSweepRight, 0, A.l, A.r, B.l, B.r,
+                        0.0, 0};
+      keep.push_back(A.b);
+      keep.push_back(B.b);
+      c.s[i] = nA;
+      c.s[i + 1] = nB;
+      ++i;
+    }
+    sweep_launch<R>(pk, max_pq, max_pp);
+  }
+}
+
+// push_left for i in (to, from], descending
+template <typename R>
+static void push_left_range(mb_chain& c, int from, int to) {
+  const int d = c.d;
+  int i = from;
+  while (i > to) {
+    if (!sweep_enabled() || !fuse_left<R>(c, i)) {
+      push_left<R>(c, i);
+      --i;
+      continue;
+    }
+    SweepPack<R> pk = sweep_pack<R>(d);
+    std::vector<Buf> keep;
+    int64_t max_pq = 0, max_pp = 0;
+    while (i > to && pk.n < kSweepMax && fuse_left<R>(c, i)) {
+      Site A = c.s[i], Pv = c.s[i - 1];
+      const int64_t m = A.l, n = (int64_t)d * A.r, k = std::min(m, n);
+      Site nA = new_site<R>(k, d, A.r), nP = new_site<R>(Pv.l, d, k);
+      if (m <= n) {
+        max_pq = std::max(max_pq, m * n);
+        max_pp = std::max(max_pp, m * m);
+      }
+      SweepStep<R>& st = pk.st[pk.n++];
+      st = SweepStep<R>{P<R>(A), P<R>(Pv), P<R>(nA), P<R>(nP), kSweepLeft, 0, A.l, A.r, Pv.l, Pv.r,
+                        0.0, 0};
+      keep.push_back(A.b);
+      keep.push_back(Pv.b);
+      c.s[i] = nA;
+      c.s[i - 1] = nP;
+      --i;
+    }
+    sweep_launch<R>(pk, max_pq, max_pp);
+  }
+}
+
 template <typename R>
 static void move_center(mb_chain& c, int target) {
   require(target >= 0 && target < c.n, "center target out of range");
   if (c.center < 0) {
-    for (int i = 0; i < target; ++i) push_right<R>(c, i);
-    for (int i = c.n - 1; i > target; --i) push_left<R>(c, i);
+    push_right_range<R>(c, 0, target);
+    push_left_range<R>(c, c.n - 1, target);
   } else if (c.center < target) {
-    for (int i = c.center; i < target; ++i) push_right<R>(c, i);
+    push_right_range<R>(c, c.center, target);
   } else {
-    for (int i = c.center; i > target; --i) push_left<R>(c, i);
+    push_left_range<R>(c, c.center, target);
   }
   c.center = target;
 }
@@ -733,10 +899,74 @@ static void scale_site0(mb_chain& c, double f) {
   launch_scale<R>(P<R>(c.s[0]), ne, 1.0 / f, E.stream);
 }
 
+// Truncation half of compress (chains.py:275-281) for i = n-1 .. 1: runs of
+// small steps go through k_sweep with the kept ranks decided on the device
+// and read back once per run; the new sites are allocated at their largest
+// possible rank and given their final dims after the readback.
+template <typename R>
+static void truncate_sweep(mb_chain& c, double eps, int64_t chi) {
+  const int d = c.d;
+  int i = c.n - 1;
+  while (i > 0) {
+    auto fusable = [&](int s, int64_t rcap) {
+      const Site& Pv = c.s[s - 1];
+      const int64_t m = c.s[s].l, ncap = (int64_t)d * rcap;
+      const int64_t kcap = std::min(std::min(m, ncap), chi);
+      return fuse_svd(m, ncap) && Pv.l * d * kcap * m <= kSweepGemmMax;
+    };
+    if (!sweep_enabled() || !fusable(i, c.s[i].r)) {
+      truncate_left<R>(c, i, eps, chi);
+      --i;
+      continue;
+    }
+    SweepPack<R> pk = sweep_pack<R>(d);
+    std::vector<Buf> keep;
+    struct Out {
+      int site;
+      Buf a, p;
+      int64_t r, pl;
+    };
+    std::vector<Out> outs;
+    int64_t max_pq = 0, max_pp = 0;
+    int64_t rcap = c.s[i].r;
+    while (i > 0 && pk.n < kSweepMax && fusable(i, rcap)) {
+      Site A = c.s[i], Pv = c.s[i - 1];
+      const int64_t m = A.l, ncap = (int64_t)d * rcap;
+      const int64_t pcap = std::min(m, ncap), kcap = std::min(pcap, chi);
+      max_pq = std::max(max_pq, m * ncap);
+      max_pp = std::max(max_pp, pcap * pcap);
+      Site nA = new_site<R>(kcap, d, rcap), nP = new_site<R>(Pv.l, d, kcap);
+      SweepStep<R>& st = pk.st[pk.n];
+      st = SweepStep<R>{pk.n == 0 ? P<R>(A) : nullptr, P<R>(Pv), P<R>(nA), P<R>(nP), kSweepTrunc,
+                        pk.n == 0 ? 0 : 1, m, rcap, Pv.l, Pv.r, eps, chi};
+      ++pk.n;
+      keep.push_back(A.b);
+      keep.push_back(Pv.b);
+      outs.push_back(Out{i, nA.b, nP.b, rcap, Pv.l});
+      rcap = kcap;
+      --i;
+    }
+    sweep_launch<R>(pk, max_pq, max_pp);
+    d2h(E.h_sw_info, E.sw_info->p, sizeof(int64_t) * 3 * pk.n);
+    sync();
+    // final dims: site s = (k_t, d, r_t) with r_t the previous step's rank
+    int64_t rprev = outs[0].r;
+    for (int t = 0; t < pk.n; ++t) {
+      const int64_t k = E.h_sw_info[3 * t];
+      if (E.h_sw_info[3 * t + 1]) E.counters[4]++;
+      E.counters[2] += E.h_sw_info[3 * t + 2];
+      c.s[outs[t].site] = Site{outs[t].a, k, rprev};
+      rprev = k;
+    }
+    const Out& last = outs.back();
+    c.s[last.site - 1] = Site{last.p, last.pl, rprev};
+  }
+}
+
 template <typename R>
 static void compress(mb_chain& c, double eps, int64_t chi) {
-  for (int i = 0; i + 1 < c.n; ++i) push_right<R>(c, i);
-  for (int i = c.n - 1; i > 0; --i) truncate_left<R>(c, i, eps, chi);
+  push_right_range<R>(c, 0, c.n - 1);
+  truncate_sweep<R>(c, eps, chi);
   Site A = c.s[0];
   double f = norm_of<R>(P<R>(A), A.l * c.d * A.r);
   if (f == 0.0) throw MbError(MB_ERR_NUMERIC, "compress reached an all-zero chain");
@@ -1007,11 +1237,14 @@ int mb_init(int device) {
     ck(cudaMallocHost(&E.h_disc, sizeof(double) * Engine::kSlots), "pinned");
     ck(cudaMallocHost(&E.h_scalar, sizeof(double) * 4), "pinned");
     ck(cudaMallocHost(&E.h_flag, sizeof(int) * 4), "pinned");
+    ck(cudaMallocHost(&E.h_sw_info, sizeof(int64_t) * 3 * kSweepMax), "pinned");
     E.device = device;
     E.d_info = alloc(sizeof(int64_t) * 3 * Engine::kSlots);
     E.d_disc = alloc(sizeof(double) * Engine::kSlots);
     E.d_flag = alloc(sizeof(int) * 4);
     E.d_scalar = alloc(sizeof(double) * 4);
+    E.sw_info = alloc(sizeof(int64_t) * 3 * kSweepMax);
+    E.sw_disc = alloc(sizeof(double) * kSweepMax);
     E.ready = true;
     ck(cudaStreamSynchronize(E.stream), "init sync");
     return 0;

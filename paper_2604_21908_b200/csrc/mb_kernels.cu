@@ -256,6 +256,9 @@ struct PairSmem {
   cx<R> ph[W2 / 2];
   int pj[W2 / 2], pk[W2 / 2];
   int col[W2];
+  R sv[W2];    // sorted singular values (small path)
+  int pv[W2];  // sorted slot -> source column
+  int64_t rank;
   int flag;
 };
 
@@ -514,14 +517,14 @@ struct JobPack {
   SvdJob<R> j[kPackJobs];
 };
 
-template <typename R, int W2, int NT>
-__global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
-  const SvdJob<R> J = pack.j[blockIdx.x];
+// Whole small SVD of one job by one CTA: init, Gram / EVD / rotation loop,
+// column norms -> sorted sigma + permutation, the truncation rule. Writes
+// J.sig, J.perm, J.info, J.disc (visible to the CTA after the final barrier).
+template <typename R, int W2>
+__device__ void small_svd_body(PairSmem<R, W2>& S, const SvdJob<R>& J) {
+  __shared__ R sg[W2];
   const int64_t p = J.m < J.n ? J.m : J.n;
   const int64_t q = J.m < J.n ? J.n : J.m;
-  if (p > W2) return;
   if (J.A) job_init(J, p, q);
   for (int c = threadIdx.x; c < W2; c += blockDim.x) S.col[c] = c < p ? c : -1;
   __syncthreads();
@@ -537,7 +540,6 @@ __global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
   }
   if (!converged) pair_gram<R, W2>(S, J.X, q);
   // column norms from the final Gram diagonal; rank-by-count sort (desc, stable)
-  __shared__ R sg[W2];
   for (int c = threadIdx.x; c < W2; c += blockDim.x) {
     R d = c < p ? S.h[c][c].x : (R)0;
     sg[c] = d > 0 ? sqrt(d) : (R)0;
@@ -552,18 +554,175 @@ __global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
     }
     J.sig[pos] = v;
     J.perm[pos] = c;
+    S.sv[pos] = v;
+    S.pv[pos] = c;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    // re-read sorted values (global, written by this block)
-    __threadfence_block();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    rank_rule<R>(J.sig, (int)p, J.eps, J.chi, &J.info[0], J.disc);
+  if (threadIdx.x == 0) {  // from shared memory: the global copies are for other kernels
+    int64_t rk;
+    double disc;
+    rank_rule<R>(S.sv, (int)p, J.eps, J.chi, &rk, &disc);
+    S.rank = rk;
+    J.info[0] = rk;
+    *J.disc = disc;
     J.info[1] = converged ? 0 : 1;
     J.info[2] = it;
   }
+  __syncthreads();
+}
+
+template <typename R, int W2, int NT>
+__global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  const SvdJob<R> J = pack.j[blockIdx.x];
+  const int64_t p = J.m < J.n ? J.m : J.n;
+  if (p > W2) return;
+  small_svd_body<R, W2>(S, J);
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident canonical-form sweeps (chains.py:110-125 and the truncation
+// half of compress, chains.py:275-281): one CTA walks a run of consecutive
+// site steps, each an SVD split whose factors are written straight into the
+// new site tensors and whose carry is multiplied into the neighbour, with
+// the truncation ranks decided and consumed on the device. A run replaces
+// three launches and (for truncations) one host round trip per site.
+// ---------------------------------------------------------------------------
+
+// out (M x N, ldo) = Lm (M x K, ldl) @ Rm (K x N, ldr), all row-major, by one CTA.
+template <typename R>
+__device__ void cta_gemm(cx<R>* __restrict__ out, int64_t ldo, const cx<R>* Lm, int64_t ldl,
+                         const cx<R>* Rm, int64_t ldr, int64_t M, int64_t N, int64_t K) {
+  for (int64_t e = threadIdx.x; e < M * N; e += blockDim.x) {
+    const int64_t i = e / N, j = e % N;
+    cx<R> acc = mk<R>(0, 0);
+    for (int64_t t = 0; t < K; ++t) cfma(acc, Lm[i * ldl + t], Rm[t * ldr + j]);
+    out[i * ldo + j] = acc;
+  }
+}
+
+// One SVD split of a sweep step with the W2-wide small-SVD body (W2 >= p):
+// factors written as in k_emit, carry multiplied into the neighbour. Returns
+// the kept rank.
+template <typename R, int W2>
+__device__ int64_t sweep_split(unsigned char* smem_raw, const SweepPack<R>& pk, int s,
+                               const SweepStep<R>& st, const cx<R>* A, int64_t m, int64_t n) {
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  const int d = pk.d;
+  const bool right = st.kind == kSweepRight;
+  int64_t* info = pk.info + 3 * s;
+  SvdJob<R> J;
+  J.A = A;
+  J.X = pk.X;
+  J.V = pk.V;
+  J.sig = pk.sig;
+  J.perm = pk.perm;
+  J.m = m;
+  J.n = n;
+  J.eps = st.kind == kSweepTrunc ? st.eps : 0.0;
+  J.chi = st.kind == kSweepTrunc ? st.chi : (int64_t)1 << 62;
+  J.info = info;
+  J.disc = pk.disc + s;
+  J.W = nullptr;
+  small_svd_body<R, W2>(S, J);
+  if (pk.tprof && threadIdx.x == 0) pk.tprof[4 * s + 1] = clock64();
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  const bool tall = m >= n;
+  const int64_t k = st.kind == kSweepTrunc ? S.rank : p;
+  if (threadIdx.x == 0 && st.kind != kSweepTrunc) info[0] = p;
+  // factors: U-part (m x k), V-part (k x n) as in k_emit
+  cx<R>* Uo = right ? st.nA : pk.carry;  // push_right: site = U;  left/trunc: carry = U sigma
+  cx<R>* Vo = right ? pk.carry : st.nA;  // push_right: carry = sigma V^H; left/trunc: site = V^H
+  const bool su = !right, sv = right;
+  const int ki = (int)k, ni = (int)n;
+  for (int e = threadIdx.x; e < (int)(m * k + k * n); e += blockDim.x) {
+    if (e < m * k) {
+      const int i = e / ki, kk = e % ki;
+      const int src = S.pv[kk];
+      const R sg = S.sv[kk];
+      cx<R> v;
+      if (tall) {
+        v = J.X[(int64_t)src * q + i];
+        if (!su) v = sg > 0 ? cscale(v, (R)1 / sg) : mk<R>(0, 0);
+      } else {
+        v = J.V[(int64_t)src * p + i];
+        if (su) v = cscale(v, sg);
+      }
+      Uo[e] = v;
+    } else {
+      const int f = e - (int)(m * k), kk = f / ni, c = f % ni;
+      const int src = S.pv[kk];
+      const R sg = S.sv[kk];
+      cx<R> v;
+      if (tall) {
+        v = cconj(J.V[(int64_t)src * p + c]);
+        if (sv) v = cscale(v, sg);
+      } else {
+        v = cconj(J.X[(int64_t)src * q + c]);
+        if (!sv) v = sg > 0 ? cscale(v, (R)1 / sg) : mk<R>(0, 0);
+      }
+      Vo[f] = v;
+    }
+  }
+  __syncthreads();
+  if (pk.tprof && threadIdx.x == 0) pk.tprof[4 * s + 2] = clock64();
+  if (right)  // next = (sigma V^H) (k x n) @ B (n x d*br)
+    cta_gemm<R>(st.nB, d * st.br, pk.carry, n, st.B, d * st.br, k, d * st.br, n);
+  else        // prev = P (bl*d x m) @ (U sigma) (m x k)
+    cta_gemm<R>(st.nB, k, st.B, m, pk.carry, k, st.bl * d, k, m);
+  return k;
+}
+
+template <typename R, int NT>
+__global__ void __launch_bounds__(NT) k_sweep(const SweepPack<R> pk) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int d = pk.d;
+  int64_t kprev = 0;
+  const cx<R>* prev = nullptr;
+  for (int s = 0; s < pk.n; ++s) {
+    const SweepStep<R> st = pk.st[s];
+    if (pk.tprof && threadIdx.x == 0) pk.tprof[4 * s] = clock64();
+    const cx<R>* A = st.from_prev ? prev : st.A;
+    const int64_t l = st.l;
+    const int64_t r = (st.from_prev && st.kind == kSweepTrunc) ? kprev : st.r;
+    const bool right = st.kind == kSweepRight;
+    const int64_t m = right ? l * d : l, n = right ? r : (int64_t)d * r;
+    int64_t* info = pk.info + 3 * s;
+    if (right && m < n) {  // wide: Q = I_m, R = A (engine push_right)
+      for (int64_t e = threadIdx.x; e < m * m; e += blockDim.x)
+        st.nA[e] = mk<R>(e / m == e % m ? 1 : 0, 0);
+      cta_gemm<R>(st.nB, d * st.br, A, n, st.B, d * st.br, m, d * st.br, n);
+      if (threadIdx.x == 0) { info[0] = m; info[1] = 0; info[2] = -1; }
+      kprev = m;
+    } else if (!right && st.kind == kSweepLeft && m > n) {  // tall: Q = I_n, L = A
+      for (int64_t e = threadIdx.x; e < n * n; e += blockDim.x)
+        st.nA[e] = mk<R>(e / n == e % n ? 1 : 0, 0);
+      cta_gemm<R>(st.nB, n, st.B, m, A, n, st.bl * d, n, m);
+      if (threadIdx.x == 0) { info[0] = n; info[1] = 0; info[2] = -1; }
+      kprev = n;
+    } else {
+      const int64_t p = m < n ? m : n;
+      if (p <= 16) kprev = sweep_split<R, 16>(smem_raw, pk, s, st, A, m, n);
+      else if (p <= 32) kprev = sweep_split<R, 32>(smem_raw, pk, s, st, A, m, n);
+      else kprev = sweep_split<R, 64>(smem_raw, pk, s, st, A, m, n);
+    }
+    prev = st.nB;
+    __syncthreads();  // outputs visible to the next step
+    if (pk.tprof && threadIdx.x == 0) pk.tprof[4 * s + 3] = clock64();
+  }
+}
+
+template <typename R>
+void launch_sweep(const SweepPack<R>& pk, cudaStream_t s) {
+  static bool attr = false;
+  const size_t sm = sizeof(PairSmem<R, kSmallP>);
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep<R, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_sweep<R, 512><<<1, 512, sm, s>>>(pk);
+  MB_LAUNCH_CHECK();
 }
 
 // Small-p SVD for tall problems: the CL CTAs of a cluster split the q rows of
@@ -642,10 +801,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
       }
       J.sig[pos] = v;
       J.perm[pos] = c;
+      S.sv[pos] = v;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      rank_rule<R>(J.sig, (int)p, J.eps, J.chi, &J.info[0], J.disc);
+      rank_rule<R>(S.sv, (int)p, J.eps, J.chi, &J.info[0], J.disc);
       J.info[1] = converged ? 0 : 1;
       J.info[2] = it;
     }
@@ -687,6 +847,14 @@ void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t 
         if (CL == 8) launch_small_cl<R, 64, 8>(pack, cnt, s);
         else launch_small_cl<R, 64, 4>(pack, cnt, s);
       }
+    } else if (max_p <= 16) {
+      static bool attr16 = false;
+      size_t sm = sizeof(PairSmem<R, 16>);
+      if (!attr16) {
+        cudaFuncSetAttribute(k_svd_small<R, 16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr16 = true;
+      }
+      k_svd_small<R, 16, 256><<<cnt, 256, sm, s>>>(pack);
     } else if (max_p <= 32) {
       size_t sm = sizeof(PairSmem<R, 32>);
       if (!attr32) {
@@ -1629,6 +1797,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_qr_emit<R>(const cx<R>*, const cx<R>*, int64_t, int64_t, bool, cx<R>*,   \
                                   cx<R>*, cudaStream_t);                                        \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
+  template void launch_sweep<R>(const SweepPack<R>&, cudaStream_t);                             \
   template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
                                cudaStream_t);                                                   \
   template void launch_identity<R>(cx<R>*, int64_t, cudaStream_t);                              \

@@ -60,6 +60,46 @@ void launch_gate1(const cx<R>* src, cx<R>* dst, const Gate2<R>& u, int64_t l, in
 template <typename R>
 void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t s);
 
+// Device-resident run of canonical-form steps (see k_sweep). Steps are taken
+// in order by one CTA; each factors its site (p <= kSmallP) and multiplies the
+// carry into the neighbour. Truncation steps marked from_prev read the previous
+// step's neighbour output, whose column count is d * (previous kept rank).
+constexpr int kSweepRight = 0;  // push_right: A (l*d x r) = U (site) * [sigma V^H] -> into B
+constexpr int kSweepLeft = 1;   // push_left:  A (l x d*r) = [U sigma] -> into B * V^H (site)
+constexpr int kSweepTrunc = 2;  // truncate_left: as push_left with the rank rule (eps, chi)
+constexpr int kSweepMax = 48;
+
+template <typename R>
+struct SweepStep {
+  const cx<R>* A;  // site tensor (ignored when from_prev)
+  const cx<R>* B;  // neighbour: right -> site i+1 (r x d x br); left/trunc -> site i-1 (bl x d x l)
+  cx<R>* nA;       // new site (capacity for the largest possible rank)
+  cx<R>* nB;       // new neighbour
+  int kind;
+  int from_prev;
+  int64_t l, r;    // site dims (r replaced on the device for from_prev truncations)
+  int64_t bl, br;  // neighbour's outer dims
+  double eps;
+  int64_t chi;
+};
+
+template <typename R>
+struct SweepPack {
+  SweepStep<R> st[kSweepMax];
+  int n, d;
+  cx<R>* X;       // scratch p*q
+  cx<R>* V;       // scratch p*p
+  R* sig;         // 2 * kSmallP
+  int* perm;      // kSmallP
+  cx<R>* carry;   // scratch max(m*k, k*n)
+  int64_t* info;  // 3 per step: [0] kept rank, [1] not converged, [2] iterations
+  double* disc;   // per step
+  long long* tprof;  // debug: 4 clock64 stamps per step, or null
+};
+
+template <typename R>
+void launch_sweep(const SweepPack<R>& pk, cudaStream_t s);
+
 // Large SVD (p > kSmallP): host-driven block Jacobi sweeps. scratch_dev holds
 // >= 257 doubles (norm reduction).
 // (the job's X pointer is redirected to the workspace holding U*sigma)
