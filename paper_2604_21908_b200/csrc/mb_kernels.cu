@@ -13,6 +13,8 @@
 #include <cooperative_groups.h>
 
 #include <atomic>
+#include <chrono>
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -240,10 +242,15 @@ __device__ __forceinline__ double abs_floor(int64_t q) {
 }
 
 // Tournament (circle method) pairing for NP even: round rnd, pair i.
+// (0 <= rnd < NP - 1, so the modulo is one conditional subtraction)
 __device__ __forceinline__ void tournament(int NP, int rnd, int i, int& a, int& b) {
-  a = (i == 0) ? 0 : ((i - 1 + rnd) % (NP - 1)) + 1;
-  int j = NP - 1 - i;
-  b = ((j - 1 + rnd) % (NP - 1)) + 1;
+  const int M = NP - 1;
+  int x = i - 1 + rnd;
+  x = x >= M ? x - M : x;
+  a = (i == 0) ? 0 : x + 1;
+  int y = NP - 2 - i + rnd;
+  y = y >= M ? y - M : y;
+  b = y + 1;
 }
 
 template <typename R, int W2>
@@ -353,6 +360,19 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
   __syncthreads();
   const double t2 = tol * tol, f2 = floor_abs * floor_abs;
   const int npairs = np / 2;
+  // This thread's work items of every round, decoded once: (pa, pb) 2x2 blocks
+  // of h, then (row, pb) pairs of w. (Integer division by the runtime pair
+  // count inside the round loop was ~20% of the EVD's issue slots.)
+  constexpr int kItems = (3 * W2 * W2 / 4 + 255) / 256;  // blockDim >= 256
+  const int nblk = npairs * npairs, nitems = nblk + np * npairs;
+  int code[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int e = tid + k * (int)blockDim.x;
+    if (e < nblk) code[k] = (e / npairs) | ((e % npairs) << 8);
+    else if (e < nitems) code[k] = ((e - nblk) / npairs) | (((e - nblk) % npairs) << 8) | (1 << 16);
+    else code[k] = -1;
+  }
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) S.flag = 0;
     __syncthreads();
@@ -367,13 +387,15 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
         cx<R> g = S.h[j][k];
         double ga2 = (double)cabs2(g);
         if (a > 0 && b > 0 && ga2 > t2 * a * b && ga2 > f2 * (a > b ? a : b)) {
-          double ga = sqrt(ga2);
-          double zeta = (b - a) / (2.0 * ga);
-          double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          double c = 1.0 / sqrt(1.0 + t * t);
+          // one division and three square roots on the dependent chain
+          // (rsqrt + multiplies instead of five divisions)
+          const double inv_ga = rsqrt(ga2);
+          const double zeta = 0.5 * (b - a) * inv_ga;
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(t, t, 1.0));
           S.cs[tid] = (R)c;
           S.sn[tid] = (R)(c * t);
-          S.ph[tid] = mk<R>((R)(g.x / ga), (R)(-g.y / ga));  // e^{-i phi}
+          S.ph[tid] = mk<R>((R)(g.x * inv_ga), (R)(-g.y * inv_ga));  // e^{-i phi}
           S.flag = 1;
         } else {
           S.cs[tid] = 1;
@@ -382,11 +404,13 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
         }
       }
       __syncthreads();
-      // h blocks: npairs x npairs 2x2 blocks
-      const int nblk = npairs * npairs;
-      for (int e = tid; e < nblk + np * npairs; e += blockDim.x) {
-        if (e < nblk) {
-          const int pa = e / npairs, pb = e % npairs;
+      // h blocks: npairs x npairs 2x2 blocks; then the rows of w
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int cd = code[it];
+        if (cd < 0) continue;
+        if (!(cd >> 16)) {
+          const int pa = cd & 255, pb = (cd >> 8) & 255;
           const R ca = S.cs[pa], sa = S.sn[pa], cb = S.cs[pb], sb = S.sn[pb];
           if (sa == 0 && sb == 0) continue;
           const int ja = S.pj[pa], ka = S.pk[pa], jb = S.pj[pb], kb = S.pk[pb];
@@ -406,7 +430,7 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
           S.h[ka][jb] = csub(cscale(t10, cb), cscale(f11, sb));
           S.h[ka][kb] = cadd(cscale(t10, sb), cscale(f11, cb));
         } else {
-          const int f = e - nblk, rr = f / npairs, pb = f % npairs;
+          const int rr = cd & 255, pb = (cd >> 8) & 255;
           const R cb = S.cs[pb], sb = S.sn[pb];
           if (sb == 0) continue;
           const int jb = S.pj[pb], kb = S.pk[pb];
@@ -456,6 +480,7 @@ template <typename R>
 __device__ void rank_rule(const R* sig, int p, double eps, int64_t chi, int64_t* rank_out,
                           double* disc_out) {
   double total = 0;
+#pragma unroll 8
   for (int k = 0; k < p; ++k) total += (double)sig[k] * (double)sig[k];
   double budget = eps * eps * total;
   // suffix sums from the end, as numpy's reversed cumsum
@@ -1042,8 +1067,14 @@ __global__ void k_sort_desc(const R* __restrict__ vals, int64_t p, R* __restrict
 
 template <typename R>
 __global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    rank_rule<R>(J.sig, (int)p, J.eps, J.chi, &J.info[0], J.disc);
+  // stage the sorted spectrum in shared memory: the serial rule then runs on
+  // shared-memory latency instead of one L2 round trip per value
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* ss = reinterpret_cast<R*>(smem_raw);
+  for (int64_t i = threadIdx.x; i < p; i += blockDim.x) ss[i] = J.sig[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    rank_rule<R>(ss, (int)p, J.eps, J.chi, &J.info[0], J.disc);
     J.info[1] = conv ? 0 : 1;
     J.info[2] = sweeps;
   }
@@ -1288,6 +1319,30 @@ static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int
   MB_LAUNCH_CHECK();
 }
 
+// debug (MB_SVD_LOG): host-side phase timing of the large path
+struct PhaseLog {
+  FILE* f = nullptr;
+  std::chrono::steady_clock::time_point t;
+  cudaStream_t s;
+  explicit PhaseLog(cudaStream_t st) : s(st) {
+    static FILE* g = getenv("MB_SVD_LOG")
+                         ? fopen((std::string(getenv("MB_SVD_LOG")) + ".phase").c_str(), "w")
+                         : nullptr;
+    f = g;
+    if (f) {
+      cudaStreamSynchronize(s);
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const char* what) {
+    if (!f) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    fprintf(f, "%s %.1f\n", what, std::chrono::duration<double, std::micro>(now - t).count());
+    t = now;
+  }
+};
+
 // Block one-sided Jacobi sweeps on the column-major Xw (p columns of length
 // len) until no pair rotates. Returns (converged, sweeps).
 template <typename R>
@@ -1380,16 +1435,20 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
   static const int allow_pre = env_int("MB_JACOBI_QR", 0);
   const int precond = allow_pre && J.W != nullptr && (J.V == nullptr || J.eps >= 1e-6);
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
+  PhaseLog plog(s);
   if (J.A) {
     int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
     k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, precond ? nullptr : J.V, J.m, J.n);
     MB_LAUNCH_CHECK();
   }
+  plog.mark("init");
   int conv = 0, sweeps = 0;
   if (!precond) {
     jacobi_sweeps<R>(J.X, J.V, p, q, flag_dev, flag_host, scratch_dev, s, conv, sweeps);
+    plog.mark(sweeps ? "sweeps" : "check");
     k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(J.X, p, q, J.sig + p);
     MB_LAUNCH_CHECK();
+    plog.mark("colnorms");
   } else {
     // 1. X0 = Q R (Householder, in the workspace copy)
     cx<R>* Xq = J.W;
@@ -1464,7 +1523,17 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
   }
   k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
   MB_LAUNCH_CHECK();
-  k_rank<R><<<1, 32, 0, s>>>(J, p, conv, sweeps + 1);
+  plog.mark("sort");
+  {
+    const size_t sm = (size_t)p * sizeof(R);
+    static size_t attr = 48 * 1024;
+    if (sm > attr) {
+      cudaFuncSetAttribute(k_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = sm;
+    }
+    k_rank<R><<<1, 256, sm, s>>>(J, p, conv, sweeps + 1);
+  }
+  plog.mark("rank");
   MB_LAUNCH_CHECK();
 }
 
