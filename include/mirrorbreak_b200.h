@@ -109,6 +109,21 @@ int mb_batch_swap_extents(mb_chain* c, int nb, const int* bonds, const int* mine
 /* Two-sided sweep: orthogonalize left->right, truncate right->left,
  * renormalize into log_norm; center ends at 0.                 chains.py:262-285 */
 int mb_compress(mb_chain* c, double eps, int64_t chi_max);
+/* One adaptive-side trial in place (driver.py:178-184, _trial_absorb): absorb
+ * a layer of ng gates on `side`, then compress. Gate t: kinds[t] = 1 (single
+ * qubit qubits[t], 2x2 matrix in mats[32t .. 32t+8)) or 2 (adjacent pair with
+ * lower site qubits[t], 4x4 (out_lo,out_hi,in_lo,in_hi) matrix in
+ * mats[32t .. 32t+32)), interleaved complex doubles. */
+int mb_trial(mb_chain* c, int ng, const int* kinds, const int* qubits, const double* mats,
+             int side, double eps, int64_t chi_max);
+/* Both trials of an adaptive step (driver.py:207-208): layer L absorbed on the
+ * top legs of one clone of c, layer R on the bottom legs of another, each
+ * compressed; the two run concurrently on two streams. Returns two new
+ * handles (free with mb_chain_free). */
+int mb_trial_pair(const mb_chain* c, int nl, const int* kinds_l, const int* qubits_l,
+                  const double* mats_l, int nr, const int* kinds_r, const int* qubits_r,
+                  const double* mats_r, double eps, int64_t chi_max, mb_chain** out_l,
+                  mb_chain** out_r);
 /* Frobenius norm of the stored chain (log_norm excluded).      chains.py:95-102 */
 int mb_frobenius_norm(const mb_chain* c, double* out);
 /* All-zero input column, compressed and normalized (MPS, d=2). chains.py:293-324 */

@@ -20,6 +20,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mb_kernels.cuh"
@@ -79,7 +80,13 @@ struct Engine {
   std::vector<cudaEvent_t> pool;
 };
 
-static Engine E;
+// Two engine contexts (stream + scratch + readback buffers each): the main
+// one, and an auxiliary one that runs the second trial of the adaptive side
+// choice concurrently (mb_trial_pair). Every engine routine works on the
+// calling thread's context.
+static Engine g_main, g_aux;
+static thread_local Engine* g_cur = &g_main;
+#define E (*g_cur)
 
 DevBuf::~DevBuf() {
   if (p) cudaFreeAsync(p, s ? s : E.stream);
@@ -1182,6 +1189,114 @@ static void svd_host(const double* a, int64_t m, int64_t n, double eps, int64_t 
   for (int64_t i = 0; i < k; ++i) s[i] = (double)sg[i];
 }
 
+// Create the calling thread's context (stream, pinned readback buffers,
+// device scalars) on `device`.
+static void init_context(int device) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaMallocHost(&E.h_info, sizeof(int64_t) * 3 * Engine::kSlots), "pinned");
+  ck(cudaMallocHost(&E.h_disc, sizeof(double) * Engine::kSlots), "pinned");
+  ck(cudaMallocHost(&E.h_scalar, sizeof(double) * 4), "pinned");
+  ck(cudaMallocHost(&E.h_flag, sizeof(int) * 4), "pinned");
+  ck(cudaMallocHost(&E.h_sw_info, sizeof(int64_t) * 3 * kSweepMax), "pinned");
+  E.device = device;
+  E.d_info = alloc(sizeof(int64_t) * 3 * Engine::kSlots);
+  E.d_disc = alloc(sizeof(double) * Engine::kSlots);
+  E.d_flag = alloc(sizeof(int) * 4);
+  E.d_scalar = alloc(sizeof(double) * 4);
+  E.sw_info = alloc(sizeof(int64_t) * 3 * kSweepMax);
+  E.sw_disc = alloc(sizeof(double) * kSweepMax);
+  E.ready = true;
+  ck(cudaStreamSynchronize(E.stream), "init sync");
+}
+
+// ---- trial absorptions (driver.py:178-208) ---------------------------------
+
+// One adaptive-side trial on `c` (already a clone): absorb the layer's gates
+// on `side`, then compress (driver.py:178-184). Gate t: kinds[t] = 1 (one
+// qubit, 2x2 matrix in mats[32t:32t+8]) or 2 (adjacent pair with lower site
+// qubits[t], 4x4 matrix in mats[32t:32t+32]), interleaved complex.
+template <typename R>
+static void trial(mb_chain& c, int ng, const int* kinds, const int* qubits, const double* mats,
+                  int side, double eps, int64_t chi) {
+  for (int t = 0; t < ng; ++t) {
+    if (kinds[t] == 1) absorb_1q<R>(c, qubits[t], mats + 32 * t, side);
+    else if (kinds[t] == 2) absorb_2q<R>(c, qubits[t], mats + 32 * t, side, eps, chi);
+    else throw MbError(MB_ERR_ARG, "gate kind must be 1 or 2");
+  }
+  compress<R>(c, eps, chi);
+}
+
+// Both trials of one adaptive step at once: `l` on the main context (this
+// thread), `r` on the auxiliary context (a second thread and stream). The
+// two trials share the input chain's site buffers read-only. Afterwards the
+// auxiliary stream is drained and every buffer it allocated for `r` is
+// handed to the main stream, so later frees stay stream-ordered with the
+// main stream's users.
+template <typename R>
+static void trial_pair(mb_chain& l, int nl, const int* kl, const int* ql, const double* ml,
+                       mb_chain& r, int nr, const int* kr, const int* qr, const double* mr,
+                       double eps, int64_t chi) {
+  Engine& M = g_main;
+  if (!g_aux.ready) {
+    g_cur = &g_aux;
+    try {
+      init_context(M.device);
+    } catch (...) {
+      g_cur = &M;
+      throw;
+    }
+    g_cur = &M;
+  }
+  Engine& A = g_aux;
+  // the input chain's pending producers are on the main stream
+  cudaEvent_t ready_ev;
+  ck(cudaEventCreateWithFlags(&ready_ev, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(ready_ev, M.stream), "event record");
+  ck(cudaStreamWaitEvent(A.stream, ready_ev, 0), "stream wait");
+  A.prof = M.prof;
+  std::string aux_err;
+  int aux_code = 0;
+  std::thread worker([&] {
+    g_cur = &A;
+    try {
+      ck(cudaSetDevice(A.device), "cudaSetDevice");
+      trial<R>(r, nr, kr, qr, mr, MB_SIDE_RIGHT, eps, chi);
+    } catch (const MbError& e) {
+      aux_err = e.what();
+      aux_code = e.code;
+    } catch (const std::exception& e) {
+      aux_err = e.what();
+      aux_code = MB_ERR_ARG;
+    }
+  });
+  std::string main_err;
+  int main_code = 0;
+  try {
+    trial<R>(l, nl, kl, ql, ml, MB_SIDE_LEFT, eps, chi);
+  } catch (const MbError& e) {
+    main_err = e.what();
+    main_code = e.code;
+  } catch (const std::exception& e) {
+    main_err = e.what();
+    main_code = MB_ERR_ARG;
+  }
+  worker.join();
+  ck(cudaStreamSynchronize(A.stream), "aux sync");
+  cudaEventDestroy(ready_ev);
+  for (auto& st : r.s)
+    if (st.b && st.b->s == A.stream) st.b->s = M.stream;
+  for (int i = 0; i < 8; ++i) {
+    M.counters[i] += A.counters[i];
+    A.counters[i] = 0;
+  }
+  M.recs.insert(M.recs.end(), A.recs.begin(), A.recs.end());
+  A.recs.clear();
+  if (main_code) throw MbError(main_code, main_err);
+  if (aux_code) throw MbError(aux_code, aux_err);
+}
+
+
 }  // namespace mb
 
 // =============================================================================
@@ -1228,28 +1343,15 @@ int mb_init(int device) {
   MB_TRY({
     if (E.ready && E.device == device) return 0;
     ck(cudaSetDevice(device), "cudaSetDevice");
-    ck(cudaStreamCreateWithFlags(&E.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cudaMemPool_t pool;
     ck(cudaDeviceGetDefaultMemPool(&pool, device), "mempool");
     uint64_t thr = std::numeric_limits<uint64_t>::max();
     ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
-    ck(cudaMallocHost(&E.h_info, sizeof(int64_t) * 3 * Engine::kSlots), "pinned");
-    ck(cudaMallocHost(&E.h_disc, sizeof(double) * Engine::kSlots), "pinned");
-    ck(cudaMallocHost(&E.h_scalar, sizeof(double) * 4), "pinned");
-    ck(cudaMallocHost(&E.h_flag, sizeof(int) * 4), "pinned");
-    ck(cudaMallocHost(&E.h_sw_info, sizeof(int64_t) * 3 * kSweepMax), "pinned");
-    E.device = device;
-    E.d_info = alloc(sizeof(int64_t) * 3 * Engine::kSlots);
-    E.d_disc = alloc(sizeof(double) * Engine::kSlots);
-    E.d_flag = alloc(sizeof(int) * 4);
-    E.d_scalar = alloc(sizeof(double) * 4);
-    E.sw_info = alloc(sizeof(int64_t) * 3 * kSweepMax);
-    E.sw_disc = alloc(sizeof(double) * kSweepMax);
-    E.ready = true;
-    ck(cudaStreamSynchronize(E.stream), "init sync");
+    init_context(device);
     return 0;
   });
 }
+
 
 void* mb_stream(void) { return (void*)E.stream; }
 
@@ -1425,6 +1527,36 @@ int mb_compress(mb_chain* c, double eps, int64_t chi) {
     require(eps >= 0 && chi >= 1, "bad truncation parameters");
     if (c->dtype == MB_C64) compress<float>(*c, eps, chi);
     else compress<double>(*c, eps, chi);
+    return 0;
+  });
+}
+
+int mb_trial(mb_chain* c, int ng, const int* kinds, const int* qubits, const double* mats, int side,
+             double eps, int64_t chi) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    require(side == MB_SIDE_LEFT || side == MB_SIDE_RIGHT, "side must be left or right");
+    if (c->dtype == MB_C64) trial<float>(*c, ng, kinds, qubits, mats, side, eps, chi);
+    else trial<double>(*c, ng, kinds, qubits, mats, side, eps, chi);
+    return 0;
+  });
+}
+
+int mb_trial_pair(const mb_chain* c, int nl, const int* kinds_l, const int* qubits_l,
+                  const double* mats_l, int nr, const int* kinds_r, const int* qubits_r,
+                  const double* mats_r, double eps, int64_t chi, mb_chain** out_l, mb_chain** out_r) {
+  MB_TRY({
+    ensure_ready();
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    require(out_l && out_r, "null output handle");
+    std::unique_ptr<mb_chain> l(new mb_chain(*c));
+    std::unique_ptr<mb_chain> r(new mb_chain(*c));
+    if (c->dtype == MB_C64)
+      trial_pair<float>(*l, nl, kinds_l, qubits_l, mats_l, *r, nr, kinds_r, qubits_r, mats_r, eps, chi);
+    else
+      trial_pair<double>(*l, nl, kinds_l, qubits_l, mats_l, *r, nr, kinds_r, qubits_r, mats_r, eps, chi);
+    *out_l = l.release();
+    *out_r = r.release();
     return 0;
   });
 }

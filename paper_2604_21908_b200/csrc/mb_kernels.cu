@@ -740,12 +740,11 @@ __global__ void __launch_bounds__(NT) k_sweep(const SweepPack<R> pk) {
 
 template <typename R>
 void launch_sweep(const SweepPack<R>& pk, cudaStream_t s) {
-  static bool attr = false;
   const size_t sm = sizeof(PairSmem<R, kSmallP>);
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep<R, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
-  }
+  // function attributes: thread-safe one-time init (two engine contexts launch concurrently)
+  static const bool attr =
+      (cudaFuncSetAttribute(k_sweep<R, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), true);
+  (void)attr;
   k_sweep<R, 512><<<1, 512, sm, s>>>(pk);
   MB_LAUNCH_CHECK();
 }
@@ -840,19 +839,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
 
 template <typename R, int W2, int CL>
 static void launch_small_cl(const JobPack<R>& pack, int cnt, cudaStream_t s) {
-  static bool attr = false;
   size_t sm = sizeof(PairSmem<R, W2>);
-  if (!attr) {
-    cudaFuncSetAttribute(k_svd_small_cl<R, W2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    attr = true;
-  }
+  static const bool attr = (cudaFuncSetAttribute(k_svd_small_cl<R, W2, CL>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                            true);
+  (void)attr;
   k_svd_small_cl<R, W2, CL><<<cnt * CL, 256, sm, s>>>(pack);
 }
 
 template <typename R>
 void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t s) {
-  static bool attr32 = false, attr64 = false;
   static const int use_cl = getenv("MB_SMALL_CLUSTER") ? atoi(getenv("MB_SMALL_CLUSTER")) : 1;
   static const int nt64 = getenv("MB_SMALL_THREADS") ? atoi(getenv("MB_SMALL_THREADS")) : 512;
   int64_t max_q = 0;
@@ -873,27 +869,26 @@ void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t 
         else launch_small_cl<R, 64, 4>(pack, cnt, s);
       }
     } else if (max_p <= 16) {
-      static bool attr16 = false;
       size_t sm = sizeof(PairSmem<R, 16>);
-      if (!attr16) {
-        cudaFuncSetAttribute(k_svd_small<R, 16, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr16 = true;
-      }
+      static const bool attr16 = (cudaFuncSetAttribute(k_svd_small<R, 16, 256>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                                  true);
+      (void)attr16;
       k_svd_small<R, 16, 256><<<cnt, 256, sm, s>>>(pack);
     } else if (max_p <= 32) {
       size_t sm = sizeof(PairSmem<R, 32>);
-      if (!attr32) {
-        cudaFuncSetAttribute(k_svd_small<R, 32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr32 = true;
-      }
+      static const bool attr32 = (cudaFuncSetAttribute(k_svd_small<R, 32, 256>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                                  true);
+      (void)attr32;
       k_svd_small<R, 32, 256><<<cnt, 256, sm, s>>>(pack);
     } else {
       size_t sm = sizeof(PairSmem<R, 64>);
-      if (!attr64) {
-        cudaFuncSetAttribute(k_svd_small<R, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaFuncSetAttribute(k_svd_small<R, 64, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        attr64 = true;
-      }
+      static const bool attr64 =
+          (cudaFuncSetAttribute(k_svd_small<R, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+           cudaFuncSetAttribute(k_svd_small<R, 64, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+           true);
+      (void)attr64;
       if (nt64 == 512) k_svd_small<R, 64, 512><<<cnt, 512, sm, s>>>(pack);
       else k_svd_small<R, 64, 256><<<cnt, 256, sm, s>>>(pack);
     }
@@ -1306,12 +1301,10 @@ template <typename R, int W2, int CL>
 static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int NB, int rnd,
                          int* flag_dev, const double* fro2, int inner, cudaStream_t s) {
   size_t sm = sizeof(PairSmem<R, W2>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    attr = true;
-  }
+  static const bool attr = (cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, CL>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                            true);
+  (void)attr;
   // rnd < 0: convergence check of every block pair in one launch
   const int pairs = rnd < 0 ? nb * (nb - 1) / 2 : NB / 2;
   k_jacobi_pair_cl<R, W2, CL><<<pairs * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev,
@@ -1526,11 +1519,9 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
   plog.mark("sort");
   {
     const size_t sm = (size_t)p * sizeof(R);
-    static size_t attr = 48 * 1024;
-    if (sm > attr) {
-      cudaFuncSetAttribute(k_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = sm;
-    }
+    static const bool attr =
+        (cudaFuncSetAttribute(k_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true);
+    (void)attr;
     k_rank<R><<<1, 256, sm, s>>>(J, p, conv, sweeps + 1);
   }
   plog.mark("rank");

@@ -264,12 +264,10 @@ void tc_gemm_c64(int64_t M, int64_t N, int64_t K, const cx<float>* A, int64_t ld
       A, lda, M, K, A3, Mp, K3);
   k_tc_prep_b<<<(int)std::min<int64_t>((Np * K3 + thr - 1) / thr, 148 * 32), thr, 0, s>>>(
       B, ldb, K, N, B3, Np, K3);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tc_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(TcSmem));
-    attr = true;
-  }
+  static const bool attr = (cudaFuncSetAttribute(k_tc_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sizeof(TcSmem)),
+                            true);
+  (void)attr;
   dim3 grid((unsigned)(Np / TC_N), (unsigned)(Mp / TC_M));
   k_tc_gemm_tf32<<<grid, TC_THREADS, sizeof(TcSmem), s>>>(A3, K3, B3, K3, Cp, Np, K3);
   k_tc_unpad<<<(int)std::min<int64_t>((M * N + thr - 1) / thr, 148 * 32), thr, 0, s>>>(Cp, Np, M, N,

@@ -412,3 +412,16 @@ def test_config1_peaked20_matches_reference(golden):
     assert sample_output(res, 200, seed=9) == case["samples_seed9"]
     bits, p = peak_output(res)
     assert bits == case["planted_peak"] == case["top1000_seed3"][0]
+
+
+@pytest.mark.parametrize("name", ["peaked10_tau4000", "peaked12_sawtooth"])
+def test_concurrent_trials_match_sequential(golden, name):
+    """mb_trial_pair (two streams, two host threads) gives bit-identical runs
+    to the sequential per-trial path."""
+    case = _case(golden, name)
+    c = parse_qasm(case["qasm"])
+    seq = run(c, ContractionConfig(**dict(case["config"], concurrent_trials=False)))
+    par = run(c, ContractionConfig(**dict(case["config"], concurrent_trials=True)))
+    assert [(t.phase, t.unitaries_consumed, t.elements) for t in seq.trace] == \
+        [(t.phase, t.unitaries_consumed, t.elements) for t in par.trace]
+    np.testing.assert_array_equal(dense_output(seq), dense_output(par))
