@@ -269,46 +269,80 @@ struct PairSmem {
   int flag;
 };
 
-// Gram of the selected columns: h[a][b] = x_a^H x_b over all q rows.
-template <typename R, int W2>
+// Register prefetch of one TQ-row chunk of the selected columns (rows
+// [i0, min(i0+TQ, r1)) of column S.col[c]); element e = tid + k*blockDim of
+// the W2 x TQ chunk goes to pre[k]. NT = blockDim.x.
+template <typename R, int W2, int NT>
+__device__ __forceinline__ void chunk_fetch(const PairSmem<R, W2>& S, const cx<R>* __restrict__ X,
+                                            int64_t ld, int64_t i0, int64_t r1,
+                                            cx<R> (&pre)[(W2 * TQ + NT - 1) / NT]) {
+  constexpr int KP = (W2 * TQ + NT - 1) / NT;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int e = threadIdx.x + k * NT;
+    cx<R> v = mk<R>(0, 0);
+    if (e < W2 * TQ) {
+      const int c = e / TQ, t = e % TQ;
+      const int gc = S.col[c];
+      if (gc >= 0 && i0 + t < r1) v = X[(int64_t)gc * ld + i0 + t];
+    }
+    pre[k] = v;
+  }
+}
+
+template <typename R, int W2, int NT>
+__device__ __forceinline__ void chunk_store(PairSmem<R, W2>& S, const cx<R> (&pre)[(W2 * TQ + NT - 1) / NT]) {
+  constexpr int KP = (W2 * TQ + NT - 1) / NT;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int e = threadIdx.x + k * NT;
+    if (e < W2 * TQ) S.xs[e / TQ][e % TQ] = pre[k];
+  }
+}
+
+// Gram of the selected columns: h[a][b] = x_a^H x_b over rows [r0, r1). The
+// next chunk's global loads are issued before the current chunk's FMAs.
+template <typename R, int W2, int NT = 256>
 __device__ void pair_gram(PairSmem<R, W2>& S, const cx<R>* __restrict__ X, int64_t q,
                           int64_t r0 = 0, int64_t r1 = -1) {
   if (r1 < 0) r1 = q;
-  constexpr int TM = W2 / 16;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  cx<R> acc[TM][TM];
+  // 16 x TX thread tile over the W2 x W2 Gram (TX = 32 with 512 threads)
+  constexpr int TX = (NT >= 512 && W2 >= 32) ? 32 : 16;
+  constexpr int TMr = W2 / 16, TMc = W2 / TX;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const bool active = tid < 16 * TX;
+  cx<R> acc[TMr][TMc];
 #pragma unroll
-  for (int i = 0; i < TM; ++i)
+  for (int i = 0; i < TMr; ++i)
 #pragma unroll
-    for (int j = 0; j < TM; ++j) acc[i][j] = mk<R>(0, 0);
+    for (int j = 0; j < TMc; ++j) acc[i][j] = mk<R>(0, 0);
+  cx<R> pre[(W2 * TQ + NT - 1) / NT];
+  if (r0 < r1) chunk_fetch<R, W2, NT>(S, X, q, r0, r1, pre);
   for (int64_t i0 = r0; i0 < r1; i0 += TQ) {
-    for (int e = tid; e < W2 * TQ; e += blockDim.x) {
-      int c = e / TQ, t = e % TQ;
-      int gc = S.col[c];
-      S.xs[c][t] = (gc >= 0 && i0 + t < r1) ? X[(int64_t)gc * q + i0 + t] : mk<R>(0, 0);
-    }
+    chunk_store<R, W2, NT>(S, pre);
     __syncthreads();
-    if (tid < 256) {  // 16 x 16 thread tile; extra threads only stage rows
+    if (i0 + TQ < r1) chunk_fetch<R, W2, NT>(S, X, q, i0 + TQ, r1, pre);
+    if (active) {
 #pragma unroll 4
-    for (int t = 0; t < TQ; ++t) {
-      cx<R> a[TM], b[TM];
+      for (int t = 0; t < TQ; ++t) {
+        cx<R> a[TMr], b[TMc];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = S.xs[ty + 16 * i][t];
+        for (int i = 0; i < TMr; ++i) a[i] = S.xs[ty + 16 * i][t];
 #pragma unroll
-      for (int j = 0; j < TM; ++j) b[j] = S.xs[tx + 16 * j][t];
+        for (int j = 0; j < TMc; ++j) b[j] = S.xs[tx + TX * j][t];
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TMr; ++i)
 #pragma unroll
-        for (int j = 0; j < TM; ++j) cfmac(acc[i][j], a[i], b[j]);
-    }
+          for (int j = 0; j < TMc; ++j) cfmac(acc[i][j], a[i], b[j]);
+      }
     }
     __syncthreads();
   }
-  if (tid < 256)
+  if (active)
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TMr; ++i)
 #pragma unroll
-      for (int j = 0; j < TM; ++j) S.h[ty + 16 * i][tx + 16 * j] = acc[i][j];
+      for (int j = 0; j < TMc; ++j) S.h[ty + 16 * i][tx + TX * j] = acc[i][j];
   __syncthreads();
 }
 
@@ -349,7 +383,7 @@ __device__ double pair_trace(PairSmem<R, W2>& S) {
 // Each round computes the rotations of its np/2 disjoint pairs, then updates
 // every 2x2 block of h in ONE phase, h[{ja,ka},{jb,kb}] <- J_a^H h J_b, and
 // w[:, {jb,kb}] <- w J_b (two barriers per round instead of three).
-template <typename R, int W2>
+template <typename R, int W2, int NT = 256>
 __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int max_sweeps,
                         int np = W2) {
   const int tid = threadIdx.x;
@@ -363,12 +397,12 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
   // This thread's work items of every round, decoded once: (pa, pb) 2x2 blocks
   // of h, then (row, pb) pairs of w. (Integer division by the runtime pair
   // count inside the round loop was ~20% of the EVD's issue slots.)
-  constexpr int kItems = (3 * W2 * W2 / 4 + 255) / 256;  // blockDim >= 256
+  constexpr int kItems = (3 * W2 * W2 / 4 + NT - 1) / NT;  // NT = blockDim.x
   const int nblk = npairs * npairs, nitems = nblk + np * npairs;
   int code[kItems];
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
-    const int e = tid + k * (int)blockDim.x;
+    const int e = tid + k * NT;
     if (e < nblk) code[k] = (e / npairs) | ((e % npairs) << 8);
     else if (e < nitems) code[k] = ((e - nblk) / npairs) | (((e - nblk) % npairs) << 8) | (1 << 16);
     else code[k] = -1;
@@ -448,19 +482,19 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
   return max_sweeps;
 }
 
-// Y[:, cols] <- Y[:, cols] W for a column-major matrix with column length len.
-template <typename R, int W2>
+// Y[:, cols] <- Y[:, cols] W for a column-major matrix with column length len
+// (rows [r0, r1)); the next chunk is prefetched while this one is rotated.
+template <typename R, int W2, int NT = 256>
 __device__ void pair_apply(PairSmem<R, W2>& S, cx<R>* __restrict__ Y, int64_t len,
                            int64_t r0 = 0, int64_t r1 = -1) {
   const int tid = threadIdx.x;
   if (r1 < 0) r1 = len;
+  cx<R> pre[(W2 * TQ + NT - 1) / NT];
+  if (r0 < r1) chunk_fetch<R, W2, NT>(S, Y, len, r0, r1, pre);
   for (int64_t i0 = r0; i0 < r1; i0 += TQ) {
-    for (int e = tid; e < W2 * TQ; e += blockDim.x) {
-      int c = e / TQ, t = e % TQ;
-      int gc = S.col[c];
-      S.xs[c][t] = (gc >= 0 && i0 + t < r1) ? Y[(int64_t)gc * len + i0 + t] : mk<R>(0, 0);
-    }
+    chunk_store<R, W2, NT>(S, pre);
     __syncthreads();
+    if (i0 + TQ < r1) chunk_fetch<R, W2, NT>(S, Y, len, i0 + TQ, r1, pre);
     for (int e = tid; e < W2 * TQ; e += blockDim.x) {
       int c = e / TQ, t = e % TQ;
       int gc = S.col[c];
@@ -545,7 +579,7 @@ struct JobPack {
 // Whole small SVD of one job by one CTA: init, Gram / EVD / rotation loop,
 // column norms -> sorted sigma + permutation, the truncation rule. Writes
 // J.sig, J.perm, J.info, J.disc (visible to the CTA after the final barrier).
-template <typename R, int W2>
+template <typename R, int W2, int NT>
 __device__ void small_svd_body(PairSmem<R, W2>& S, const SvdJob<R>& J) {
   __shared__ R sg[W2];
   const int64_t p = J.m < J.n ? J.m : J.n;
@@ -556,14 +590,14 @@ __device__ void small_svd_body(PairSmem<R, W2>& S, const SvdJob<R>& J) {
   const double tol = rel_tol<R>(q);
   int it = 0, converged = 0;
   for (; it < 16; ++it) {
-    pair_gram<R, W2>(S, J.X, q);
+    pair_gram<R, W2, NT>(S, J.X, q);
     const double fl = abs_floor<R>(q) * sqrt(pair_trace<R, W2>(S));
     if (!pair_offdiag<R, W2>(S, tol, fl)) { converged = 1; break; }
-    pair_evd<R, W2>(S, tol, fl, kSmallEvdSweeps, (int)(p + (p & 1)));
-    pair_apply<R, W2>(S, J.X, q);
-    if (J.V) pair_apply<R, W2>(S, J.V, p);
+    pair_evd<R, W2, NT>(S, tol, fl, kSmallEvdSweeps, (int)(p + (p & 1)));
+    pair_apply<R, W2, NT>(S, J.X, q);
+    if (J.V) pair_apply<R, W2, NT>(S, J.V, p);
   }
-  if (!converged) pair_gram<R, W2>(S, J.X, q);
+  if (!converged) pair_gram<R, W2, NT>(S, J.X, q);
   // column norms from the final Gram diagonal; rank-by-count sort (desc, stable)
   for (int c = threadIdx.x; c < W2; c += blockDim.x) {
     R d = c < p ? S.h[c][c].x : (R)0;
@@ -603,7 +637,7 @@ __global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
   const SvdJob<R> J = pack.j[blockIdx.x];
   const int64_t p = J.m < J.n ? J.m : J.n;
   if (p > W2) return;
-  small_svd_body<R, W2>(S, J);
+  small_svd_body<R, W2, NT>(S, J);
 }
 
 // ---------------------------------------------------------------------------
@@ -650,7 +684,7 @@ __device__ int64_t sweep_split(unsigned char* smem_raw, const SweepPack<R>& pk, 
   J.info = info;
   J.disc = pk.disc + s;
   J.W = nullptr;
-  small_svd_body<R, W2>(S, J);
+  small_svd_body<R, W2, 512>(S, J);
   if (pk.tprof && threadIdx.x == 0) pk.tprof[4 * s + 1] = clock64();
   const int64_t p = m < n ? m : n, q = m < n ? n : m;
   const bool tall = m >= n;
