@@ -73,6 +73,10 @@ struct Engine {
   // device-resident sweep runs (k_sweep)
   Buf sw_X, sw_V, sw_sig, sw_perm, sw_carry, sw_info, sw_disc;
   int64_t* h_sw_info = nullptr;  // 3 * kSweepMax
+  // large-path pair flags / schedules (grow-only; pinned host mirror)
+  Buf lg_dev;
+  int* h_lg = nullptr;
+  int64_t h_lg_cap = 0;
   long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [6] h2d bytes, [7] d2h bytes
   // profiling
   bool prof = false;
@@ -303,9 +307,21 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
       ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * (double)p * (double)p * q);
       double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
+      const int64_t cap = large_pair_capacity(jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n);
+      if (E.h_lg_cap < cap) {
+        if (E.h_lg) {
+          ck(cudaStreamSynchronize(E.stream), "sync");
+          cudaFreeHost(E.h_lg);
+        }
+        ck(cudaMallocHost(&E.h_lg, sizeof(int) * 3 * cap), "pinned");
+        E.h_lg_cap = cap;
+      }
+      int* lg = (int*)grow(E.lg_dev, sizeof(int) * 3 * cap);
+      LargeScratch ws{reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, lg, E.h_lg, lg + cap,
+                      E.h_lg + cap};
       static FILE* llog = getenv("MB_SVD_LOG") ? fopen((std::string(getenv("MB_SVD_LOG")) + ".large").c_str(), "w") : nullptr;
       auto w0 = std::chrono::steady_clock::now();
-      svd_large<R>(jobs[i], reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, E.stream);
+      svd_large<R>(jobs[i], ws, E.stream);
       if (llog) {  // debug: shapes, sweeps and host wall time of the large path
         cudaStreamSynchronize(E.stream);
         double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();

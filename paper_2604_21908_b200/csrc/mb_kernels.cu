@@ -989,25 +989,32 @@ template <typename R, int W2, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
     k_jacobi_pair_cl(cx<R>* __restrict__ X, cx<R>* __restrict__ V, int64_t p, int64_t q, int nb,
                      int NB, int rnd, int* __restrict__ flag, const double* __restrict__ fro2,
-                     int inner_sweeps) {
+                     int inner_sweeps, int* __restrict__ open, const int* __restrict__ pairs) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   constexpr int w = W2 / 2;
+  // rnd >= 0: tournament round; rnd == -1: convergence check of every block
+  // pair (linear index -> (a, b)), open pairs flagged in open[]; rnd == -2:
+  // the explicit disjoint pair list pairs[2i], pairs[2i+1]
   int a, b;
-  const bool check_only = rnd < 0;
-  if (check_only) {  // every block pair a < b at once: linear index -> (a, b)
-    int idx = blockIdx.x / CL;
+  const bool check_only = rnd == -1;
+  const int pidx = blockIdx.x / CL;
+  if (check_only) {
+    int idx = pidx;
     a = 0;
     while (idx >= nb - 1 - a) {
       idx -= nb - 1 - a;
       ++a;
     }
     b = a + 1 + idx;
+  } else if (rnd == -2) {
+    a = pairs[2 * pidx];
+    b = pairs[2 * pidx + 1];
   } else {
-    tournament(NB, rnd, blockIdx.x / CL, a, b);
+    tournament(NB, rnd, pidx, a, b);
   }
   for (int c = threadIdx.x; c < W2; c += blockDim.x) {
     int blk = c < w ? a : b;
@@ -1036,8 +1043,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
     const double tol = rel_tol<R>(q);
     const double fl = abs_floor<R>(q) * sqrt(*fro2);
     bool rot = pair_offdiag<R, W2>(S, tol, fl);
-    if (rot && check_only) {
-      if (threadIdx.x == 0) atomicAdd(flag, 1);
+    if (check_only) {
+      if (threadIdx.x == 0) {
+        if (rot) atomicAdd(flag, 1);
+        if (open) open[pidx] = rot ? 1 : 0;
+      }
       rot = false;
     }
     if (rot) pair_evd<R, W2>(S, tol, fl, inner_sweeps);
@@ -1333,16 +1343,18 @@ static int env_int(const char* name, int dflt) {
 
 template <typename R, int W2, int CL>
 static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int NB, int rnd,
-                         int* flag_dev, const double* fro2, int inner, cudaStream_t s) {
+                         int* flag_dev, const double* fro2, int inner, cudaStream_t s,
+                         int* open = nullptr, const int* pairs = nullptr, int npairs = 0) {
   size_t sm = sizeof(PairSmem<R, W2>);
   static const bool attr = (cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, CL>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                             true);
   (void)attr;
-  // rnd < 0: convergence check of every block pair in one launch
-  const int pairs = rnd < 0 ? nb * (nb - 1) / 2 : NB / 2;
-  k_jacobi_pair_cl<R, W2, CL><<<pairs * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev,
-                                                          fro2, inner);
+  // rnd == -1: convergence check of every block pair in one launch;
+  // rnd == -2: the npairs explicit pairs
+  const int np = rnd == -1 ? nb * (nb - 1) / 2 : (rnd == -2 ? npairs : NB / 2);
+  k_jacobi_pair_cl<R, W2, CL><<<np * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev, fro2,
+                                                       inner, open, pairs);
   MB_LAUNCH_CHECK();
 }
 
@@ -1372,54 +1384,100 @@ struct PhaseLog {
 
 // Block one-sided Jacobi sweeps on the column-major Xw (p columns of length
 // len) until no pair rotates. Returns (converged, sweeps).
+int64_t large_pair_capacity(int64_t p) {
+  const int64_t nb = (p + 7) / 8;  // smallest block width in use (W2 = 16)
+  return nb * (nb - 1) / 2 + 1;
+}
+
+// Block one-sided Jacobi on the column-major Xw (p columns of length len)
+// with dynamic ordering: a check launch tests every block pair at once and
+// flags the open ones; the host packs the open pairs greedily into rounds of
+// disjoint pairs and launches only those; repeat until no pair is open. A
+// first pass over a fresh matrix costs about one tournament sweep; later
+// passes touch only what is still open.
 template <typename R>
-static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, int* flag_dev,
-                          int* flag_host, double* scratch_dev, cudaStream_t s, int& conv,
-                          int& sweeps) {
-  static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : 32;
+static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const LargeScratch& ws,
+                          cudaStream_t s, int& conv, int& sweeps) {
+  static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : (env_int("MB_JACOBI_W2", 32) == 16 ? 16 : 32);
   static const int inner = env_int("MB_JACOBI_INNER", 1);
   static const int debug = env_int("MB_JACOBI_DEBUG", 0);
+  static const int dynamic = env_int("MB_JACOBI_DYNAMIC", 1);
   const int w = W2 / 2;
   // ||Xw||_F^2 (rotation-invariant) for the backward-stability floor
-  double* fro2 = scratch_dev + kSumBlocks;
-  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(Xw, p * len, scratch_dev);
+  double* fro2 = ws.red_dev + kSumBlocks;
+  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(Xw, p * len, ws.red_dev);
   MB_LAUNCH_CHECK();
-  k_sumsq_final<<<1, 256, 0, s>>>(scratch_dev, kSumBlocks, fro2);
+  k_sumsq_final<<<1, 256, 0, s>>>(ws.red_dev, kSumBlocks, fro2);
   MB_LAUNCH_CHECK();
   const int nb = (int)cdiv(p, w);
   const int NB = nb + (nb & 1);
+  const int npair = nb * (nb - 1) / 2;
   // 8-CTA clusters when the pairs alone cannot fill the chip
   const bool wide = (NB / 2) * 4 < 148 && len >= 8 * 64;
   conv = 0;
   sweeps = 0;
-  auto round = [&](int rnd) {
+  auto round = [&](int rnd, int* open, const int* pairs, int n) {
     if (W2 == 64) {
-      if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
-      else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+      if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+      else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+    } else if (W2 == 16) {
+      if (wide) launch_round<R, 16, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+      else launch_round<R, 16, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
     } else {
-      if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
-      else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, flag_dev, fro2, inner, s);
+      if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+      else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
     }
   };
-  // Convergence is tested by one all-pairs check launch (block pairs in
-  // parallel, no rotation) before each tournament sweep: inputs that are
-  // already column-orthogonal (frequent in the contraction: canonical-form
-  // moves over flat operator spectra) cost one launch, and the confirming
-  // sweep of the classic loop becomes one launch instead of NB - 1.
+  std::vector<int> pa, pb, used(nb);
+  std::vector<int> round_start;
   for (;;) {
-    cudaMemsetAsync(flag_dev, 0, sizeof(int), s);
-    round(-1);
-    cudaMemcpyAsync(flag_host, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaMemsetAsync(ws.flag_dev, 0, sizeof(int), s);
+    round(-1, dynamic ? ws.open_dev : nullptr, nullptr, 0);
+    cudaMemcpyAsync(ws.flag_host, ws.flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (dynamic) cudaMemcpyAsync(ws.open_host, ws.open_dev, sizeof(int) * npair, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    if (debug) fprintf(stderr, "[svd_large p=%lld len=%lld] after %d sweeps: %d of %d pairs open\n",
-                       (long long)p, (long long)len, sweeps, *flag_host, nb * (nb - 1) / 2);
-    if (*flag_host == 0) {
+    const int nopen = *ws.flag_host;
+    if (debug) fprintf(stderr, "[svd_large p=%lld len=%lld] after %d passes: %d of %d pairs open\n",
+                       (long long)p, (long long)len, sweeps, nopen, npair);
+    if (nopen == 0) {
       conv = 1;
       break;
     }
     if (sweeps == 60) break;
-    for (int rnd = 0; rnd < NB - 1; ++rnd) round(rnd);
     ++sweeps;
+    if (!dynamic || 2 * nopen > npair) {  // most pairs open: a full tournament sweep
+      for (int rnd = 0; rnd < NB - 1; ++rnd) round(rnd, nullptr, nullptr, 0);
+      continue;
+    }
+    // greedy packing of the open pairs into rounds of disjoint pairs
+    pa.clear();
+    pb.clear();
+    for (int a = 0, idx = 0; a < nb; ++a)
+      for (int b = a + 1; b < nb; ++b, ++idx)
+        if (ws.open_host[idx]) {
+          pa.push_back(a);
+          pb.push_back(b);
+        }
+    std::vector<char> done(pa.size(), 0);
+    size_t left = pa.size(), out = 0;
+    round_start.clear();
+    while (left) {
+      std::fill(used.begin(), used.end(), 0);
+      round_start.push_back((int)out);
+      for (size_t t = 0; t < pa.size(); ++t) {
+        if (done[t] || used[pa[t]] || used[pb[t]]) continue;
+        used[pa[t]] = used[pb[t]] = 1;
+        done[t] = 1;
+        ws.pairs_host[2 * out] = pa[t];
+        ws.pairs_host[2 * out + 1] = pb[t];
+        ++out;
+        --left;
+      }
+    }
+    round_start.push_back((int)out);
+    cudaMemcpyAsync(ws.pairs_dev, ws.pairs_host, sizeof(int) * 2 * out, cudaMemcpyHostToDevice, s);
+    for (size_t r = 0; r + 1 < round_start.size(); ++r)
+      round(-2, nullptr, ws.pairs_dev + 2 * round_start[r], round_start[r + 1] - round_start[r]);
   }
 }
 
@@ -1449,7 +1507,7 @@ static int count_bad(const cx<R>* x, int64_t n, cudaStream_t s) {
 }
 
 template <typename R>
-void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev, cudaStream_t s) {
+void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
   static const int dbg = env_int("MB_CHECK_SITES", 0);
   // QR preconditioning is used for values-only problems and for truncations at
   // cutoffs >= 1e-6, where every kept singular value sits far above the noise
@@ -1471,7 +1529,7 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
   plog.mark("init");
   int conv = 0, sweeps = 0;
   if (!precond) {
-    jacobi_sweeps<R>(J.X, J.V, p, q, flag_dev, flag_host, scratch_dev, s, conv, sweeps);
+    jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps);
     plog.mark(sweeps ? "sweeps" : "check");
     k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(J.X, p, q, J.sig + p);
     MB_LAUNCH_CHECK();
@@ -1527,7 +1585,7 @@ void svd_large(SvdJob<R>& J, int* flag_dev, int* flag_host, double* scratch_dev,
         }
       }
     }
-    jacobi_sweeps<R>(Z, nullptr, p, p, flag_dev, flag_host, scratch_dev, s, conv, sweeps);
+    jacobi_sweeps<R>(Z, nullptr, p, p, ws, s, conv, sweeps);
     if (dbg) {
       int bz = count_bad<R>(Z, p * p, s);
       if (bz) fprintf(stderr, "[svd_large dbg] after Jacobi: Z=%d sweeps=%d\n", bz, sweeps);
@@ -1885,7 +1943,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_gate1<R>(const cx<R>*, cx<R>*, const Gate2<R>&, int64_t, int64_t, bool,   \
                                 cudaStream_t);                                                  \
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
-  template void svd_large<R>(SvdJob<R>&, int*, int*, double*, cudaStream_t);                    \
+  template void svd_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                     \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
   template void qr_explicit<R>(cx<R>*, cx<R>*, cx<R>*, int64_t, int64_t, cudaStream_t);        \
   template void launch_qr_emit<R>(const cx<R>*, const cx<R>*, int64_t, int64_t, bool, cx<R>*,   \

@@ -103,9 +103,22 @@ void launch_sweep(const SweepPack<R>& pk, cudaStream_t s);
 // Large SVD (p > kSmallP): host-driven block Jacobi sweeps. scratch_dev holds
 // >= 257 doubles (norm reduction).
 // (the job's X pointer is redirected to the workspace holding U*sigma)
+// Host/device scratch of the large path (owned by the engine context).
+struct LargeScratch {
+  int* flag_dev;       // 1
+  int* flag_host;      // 1 (pinned)
+  double* red_dev;     // >= kSumBlocks + 1 doubles (norm reduction)
+  int* open_dev;       // per block pair (nb * (nb - 1) / 2)
+  int* open_host;      // pinned, same size
+  int* pairs_dev;      // 2 per block pair (scheduled passes)
+  int* pairs_host;     // pinned, same size
+};
+
+// block-pair capacity the scratch must hold for p columns
+int64_t large_pair_capacity(int64_t p);
+
 template <typename R>
-void svd_large(SvdJob<R>& job, int* flag_dev, int* flag_host, double* scratch_dev,
-               cudaStream_t s);
+void svd_large(SvdJob<R>& job, const LargeScratch& ws, cudaStream_t s);
 
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n);
