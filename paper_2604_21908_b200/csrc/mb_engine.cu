@@ -569,7 +569,7 @@ static void sweep_launch(SweepPack<R>& pk, int64_t max_pq, int64_t max_pp) {
     cudaEventCreate(&t0);
     cudaEventCreate(&t1);
     cudaEventRecord(t0, E.stream);
-    static Buf tp = alloc(sizeof(long long) * 4 * kSweepMax);
+    static thread_local Buf tp = alloc(sizeof(long long) * 4 * kSweepMax);
     pk.tprof = (long long*)tp->p;
   }
   {

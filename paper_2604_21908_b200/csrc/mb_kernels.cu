@@ -545,19 +545,18 @@ __device__ void rank_rule(const R* sig, int p, double eps, int64_t chi, int64_t*
 }
 
 // Initialize X (column-major working matrix) and V = I for one job.
+// (small path: p * q < 2^31, 32-bit index math)
 template <typename R>
-__device__ void job_init(const SvdJob<R>& J, int64_t p, int64_t q) {
-  const int64_t m = J.m, n = J.n;
-  for (int64_t e = threadIdx.x; e < p * q; e += blockDim.x) {
-    int64_t j = e / q, i = e % q;  // column j, row i of X
-    cx<R> v;
-    if (m >= n) v = J.A[i * n + j];              // X = A^T
-    else v = cconj(J.A[j * n + i]);              // X = A^H
-    J.X[e] = v;
+__device__ void job_init(const SvdJob<R>& J, int64_t p64, int64_t q64) {
+  const int n = (int)J.n, p = (int)p64, q = (int)q64;
+  const bool tall = J.m >= J.n;
+  for (int e = threadIdx.x; e < p * q; e += blockDim.x) {
+    const int j = e / q, i = e - j * q;  // column j, row i of X
+    J.X[e] = tall ? J.A[i * n + j] : cconj(J.A[j * n + i]);  // X = A^T or A^H
   }
   if (J.V) {
-    for (int64_t e = threadIdx.x; e < p * p; e += blockDim.x) {
-      int64_t j = e / p, i = e % p;
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+      const int j = e / p, i = e - j * p;
       J.V[e] = mk<R>(i == j ? 1 : 0, 0);
     }
   }
@@ -650,14 +649,29 @@ __global__ void __launch_bounds__(NT) k_svd_small(const JobPack<R> pack) {
 // ---------------------------------------------------------------------------
 
 // out (M x N, ldo) = Lm (M x K, ldl) @ Rm (K x N, ldr), all row-major, by one CTA.
+// (sizes bounded by kSweepGemmMax: 32-bit indices; the K loop is unrolled so
+// several independent L2 loads are in flight per thread)
 template <typename R>
-__device__ void cta_gemm(cx<R>* __restrict__ out, int64_t ldo, const cx<R>* Lm, int64_t ldl,
-                         const cx<R>* Rm, int64_t ldr, int64_t M, int64_t N, int64_t K) {
-  for (int64_t e = threadIdx.x; e < M * N; e += blockDim.x) {
-    const int64_t i = e / N, j = e % N;
-    cx<R> acc = mk<R>(0, 0);
-    for (int64_t t = 0; t < K; ++t) cfma(acc, Lm[i * ldl + t], Rm[t * ldr + j]);
-    out[i * ldo + j] = acc;
+__device__ void cta_gemm(cx<R>* __restrict__ out, int64_t ldo, const cx<R>* __restrict__ Lm,
+                         int64_t ldl, const cx<R>* __restrict__ Rm, int64_t ldr, int64_t M,
+                         int64_t N, int64_t K) {
+  const int n = (int)N, k = (int)K, lo = (int)ldo, ll = (int)ldl, lr = (int)ldr;
+  const int tot = (int)(M * N);
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    const cx<R>* a = Lm + i * ll;
+    const cx<R>* b = Rm + j;
+    cx<R> acc0 = mk<R>(0, 0), acc1 = mk<R>(0, 0);
+    int t = 0;
+    for (; t + 8 <= k; t += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        cfma(acc0, a[t + u], b[(t + u) * lr]);
+        cfma(acc1, a[t + u + 1], b[(t + u + 1) * lr]);
+      }
+    }
+    for (; t < k; ++t) cfma(acc0, a[t], b[t * lr]);
+    out[i * lo + j] = cadd(acc0, acc1);
   }
 }
 
