@@ -106,6 +106,16 @@ int mb_swap_extents(mb_chain* c, int bond, int nsides, const int* sides, double 
  * report -1 (merged across ranks by an all-reduce(MAX) on the host). */
 int mb_batch_swap_extents(mb_chain* c, int nb, const int* bonds, const int* mine, int side,
                           double eps, int64_t chi_max, int64_t* baselines, int64_t* extents);
+/* One bond of greedy unswapping with a single host round trip
+ * (unswap.py:137-167 _try_bond): normalize the bond (center onto it,
+ * truncated re-split; the kept rank is *baseline), score each candidate side
+ * (0 left, 1 right, 2 both) by the truncated rank of the SWAP-ed normalized
+ * blob (extents[t]), and accept the best (lowest, earlier side on ties) iff
+ * it shrinks the bond (relaxed != 0: does not grow it). *accepted = index of
+ * the accepted side in `sides`, or -1; the chain holds the accepted (or the
+ * normalized) split with the center at bond+1. */
+int mb_try_bond(mb_chain* c, int bond, int nsides, const int* sides, double eps, int64_t chi_max,
+                int relaxed, int64_t* baseline, int64_t* extents, int* accepted);
 /* Two-sided sweep: orthogonalize left->right, truncate right->left,
  * renormalize into log_norm; center ends at 0.                 chains.py:262-285 */
 int mb_compress(mb_chain* c, double eps, int64_t chi_max);

@@ -779,6 +779,65 @@ static void pair_swap(mb_chain& c, int b, bool top, bool bottom, double eps, int
   resplit<R>(c, b, th, l, r, eps, chi);
 }
 
+// One bond of greedy unswapping in a single host round trip (unswap.py:
+// 137-167 _try_bond): normalize (center onto the bond, truncated re-split of
+// the blob: the baseline rank), then for each candidate side the SWAP-ed
+// blob of the NORMALIZED split (formed on the device from the kept factors,
+// rank read on the device) is decomposed with vectors. One read-back gives
+// every rank; the best candidate (lowest extent, earlier side on ties) is
+// accepted iff it shrinks the bond (relaxed: does not grow it), and the
+// chosen factorization — candidate or baseline — is emitted into the sites.
+// Returns the accepted candidate's index or -1.
+template <typename R>
+static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, int64_t chi,
+                    bool relaxed, int64_t* baseline, int64_t* extents) {
+  require(c.d == 4, "swap on a non-operator chain");
+  require(b >= 0 && b + 1 < c.n, "bond out of range");
+  require(ns >= 0 && ns <= 3, "0..3 sides");
+  move_center<R>(c, b);
+  int64_t l, r;
+  cx<R>* th0 = blob<R>(c, b, 0, l, r);
+  const int64_t M = 4 * l, N = 4 * r;
+  g_tag = 3;
+  SvdJob<R> jobs[4];
+  jobs[0] = make_job<R>(0, th0, M, N, eps, chi, true);
+  run_jobs<R>(&jobs[0], 1);
+  Gate4<R> sw = swap_gate<R>();
+  for (int k = 0; k < ns; ++k) {
+    const int sd = sides[k];
+    require(sd >= 0 && sd <= 2, "bad side");
+    cx<R>* th = (cx<R>*)grow(E.theta[k + 1], (size_t)(M * N) * sizeof(cx<R>));
+    {
+      ProfScope ps(P_GEMM, gemm_flops(M, N, std::min(M, N)));
+      launch_trunc_blob<R>(jobs[0], th, E.stream);
+    }
+    {
+      ProfScope ps(P_GATE, 0.0);
+      if (sd == MB_SIDE_LEFT || sd == MB_SIDE_BOTH) launch_gate2<R>(th, sw, l, r, true, E.stream);
+      if (sd == MB_SIDE_RIGHT || sd == MB_SIDE_BOTH) launch_gate2<R>(th, sw, l, r, false, E.stream);
+    }
+    g_tag = 4;
+    jobs[k + 1] = make_job<R>(k + 1, th, M, N, eps, chi, true);
+  }
+  if (ns) run_jobs<R>(jobs + 1, ns);
+  read_info(ns + 1);
+  *baseline = E.h_info[0];
+  int best = -1;
+  for (int k = 0; k < ns; ++k) {
+    extents[k] = E.h_info[3 * (k + 1)];
+    if (best < 0 || extents[k] < extents[best]) best = k;
+  }
+  const bool take = best >= 0 && (extents[best] < *baseline || (relaxed && extents[best] == *baseline));
+  const SvdJob<R>& j = take ? jobs[best + 1] : jobs[0];
+  const int64_t k = take ? extents[best] : *baseline;
+  Site nA = new_site<R>(l, 4, k), nB = new_site<R>(k, 4, r);
+  emit<R>(j, k, P<R>(nA), false, P<R>(nB), true);
+  c.s[b] = nA;
+  c.s[b + 1] = nB;
+  c.center = b + 1;
+  return take ? best : -1;
+}
+
 template <typename R>
 static void swap_extents(mb_chain& c, int b, int ns, const int* sides, double eps, int64_t chi,
                          int64_t* out) {
@@ -1534,6 +1593,18 @@ int mb_batch_swap_extents(mb_chain* c, int nb, const int* bonds, const int* mine
     require(eps >= 0 && chi >= 1, "bad truncation parameters");
     if (c->dtype == MB_C64) batch_extents<float>(*c, nb, bonds, mine, side, eps, chi, baselines, extents);
     else batch_extents<double>(*c, nb, bonds, mine, side, eps, chi, baselines, extents);
+    return 0;
+  });
+}
+
+int mb_try_bond(mb_chain* c, int bond, int nsides, const int* sides, double eps, int64_t chi,
+                int relaxed, int64_t* baseline, int64_t* extents, int* accepted) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    if (c->dtype == MB_C64)
+      *accepted = try_bond<float>(*c, bond, nsides, sides, eps, chi, relaxed != 0, baseline, extents);
+    else
+      *accepted = try_bond<double>(*c, bond, nsides, sides, eps, chi, relaxed != 0, baseline, extents);
     return 0;
   });
 }

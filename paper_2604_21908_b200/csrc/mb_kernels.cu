@@ -1731,6 +1731,83 @@ __global__ void k_emit(SvdJob<R> J, int64_t k, cx<R>* __restrict__ U, bool scale
   }
 }
 
+// Truncated product of a finished SVD job, theta_k = U_k S_k V_k^H (m x n,
+// row-major), with the kept rank k read on the device (J.info[0]): tall,
+// A = X V^H; wide, A = V X^H; summed over the k leading sorted slots. Lets the
+// unswap candidate blob be formed from the normalized split without a host
+// round trip for k (unswap.py:124-134 then :104).
+template <typename R>
+__global__ void __launch_bounds__(256) k_trunc_blob(const SvdJob<R> J, cx<R>* __restrict__ out) {
+  __shared__ cx<R> As[GBK][GBM + 1];
+  __shared__ cx<R> Bs[GBK][GBN + 1];
+  const int64_t m = J.m, n = J.n;
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  const bool tall = m >= n;
+  const int64_t K = J.info[0];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * GBM, n0 = (int64_t)blockIdx.x * GBN;
+  cx<R> acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = mk<R>(0, 0);
+  const cx<R> zero = mk<R>(0, 0);
+  for (int64_t k0 = 0; k0 < K; k0 += GBK) {
+#pragma unroll
+    for (int t = 0; t < (GBM * GBK) / 256; ++t) {
+      const int e = tid + 256 * t;
+      const int kk = e / GBM, mm = e % GBM;
+      const int64_t gk = k0 + kk, gm = m0 + mm;
+      cx<R> v = zero;
+      if (gk < K && gm < m) {
+        const int64_t src = J.perm[gk];
+        v = tall ? J.X[src * q + gm] : J.V[src * p + gm];
+      }
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < (GBN * GBK) / 256; ++t) {
+      const int e = tid + 256 * t;
+      const int kk = e / GBN, nn = e % GBN;
+      const int64_t gk = k0 + kk, gn = n0 + nn;
+      cx<R> v = zero;
+      if (gk < K && gn < n) {
+        const int64_t src = J.perm[gk];
+        v = cconj(tall ? J.V[src * p + gn] : J.X[src * q + gn]);
+      }
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < GBK; ++kk) {
+      cx<R> a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cfma(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+      if (gm < m && gn < n) out[gm * n + gn] = acc[i][j];
+    }
+}
+
+template <typename R>
+void launch_trunc_blob(const SvdJob<R>& J, cx<R>* out, cudaStream_t s) {
+  dim3 grid((unsigned)cdiv(J.n, GBN), (unsigned)cdiv(J.m, GBM));
+  k_trunc_blob<R><<<grid, 256, 0, s>>>(J, out);
+  MB_LAUNCH_CHECK();
+}
+
 template <typename R>
 void launch_emit(const SvdJob<R>& J, int64_t k, cx<R>* Uout, bool scaleU, cx<R>* Vout,
                  bool scaleV, cudaStream_t s) {
@@ -1964,6 +2041,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
                                   cx<R>*, cudaStream_t);                                        \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
   template void launch_sweep<R>(const SweepPack<R>&, cudaStream_t);                             \
+  template void launch_trunc_blob<R>(const SvdJob<R>&, cx<R>*, cudaStream_t);                   \
   template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
                                cudaStream_t);                                                   \
   template void launch_identity<R>(cx<R>*, int64_t, cudaStream_t);                              \

@@ -100,6 +100,10 @@ struct SweepPack {
 template <typename R>
 void launch_sweep(const SweepPack<R>& pk, cudaStream_t s);
 
+// theta_k = U_k S_k V_k^H of a finished job, k read from job.info[0] on the device
+template <typename R>
+void launch_trunc_blob(const SvdJob<R>& job, cx<R>* out, cudaStream_t s);
+
 // Large SVD (p > kSmallP): host-driven block Jacobi sweeps. scratch_dev holds
 // >= 257 doubles (norm reduction).
 // (the job's X pointer is redirected to the workspace holding U*sigma)

@@ -92,6 +92,22 @@ class _Work:
                                            self.cfg.chi_max, nat.i64ptr(out)), "swap extents")
         return [int(x) for x in out]
 
+    def try_bond(self, bond: int, sides) -> int:
+        """Normalize + score + accept in one device call; returns the index
+        of the accepted side in ``sides`` or -1 (baseline/extents kept in
+        ``last_scores`` for tracing)."""
+        codes = (C.c_int * max(1, len(sides)))(*(nat.SIDE[s] for s in sides))
+        base = C.c_int64()
+        ext = np.zeros(3, dtype=np.int64)
+        acc = C.c_int()
+        nat.check(nat._lib.mb_try_bond(self.m._h, bond, len(sides), codes, self.cfg.epsilon,
+                                       self.cfg.chi_max, int(self.cfg.acceptance == "relaxed"),
+                                       C.byref(base), nat.i64ptr(ext), C.byref(acc)), "try bond")
+        self.last_scores = (int(base.value), [int(x) for x in ext[:len(sides)]])
+        if acc.value < 0:
+            self.refresh()
+        return int(acc.value)
+
     def score_batch(self, bonds, mine, side):
         """Device batch scoring of one (side, parity) batch (this rank's shard)."""
         nb = len(bonds)
@@ -139,20 +155,19 @@ class _Work:
 
 
 def _try_bond(w: _Work, bond: int, sides, seen) -> bool:
-    """unswap.py:137-167: ties prefer earlier sides (left, right, both)."""
-    baseline = w.normalize(bond)
+    """unswap.py:137-167: normalize the bond, score the candidate sides on the
+    normalized split, accept the best (ties prefer earlier sides: left,
+    right, both) iff it shrinks the bond (relaxed: does not grow it). One
+    engine call (mb_try_bond), one host round trip."""
     todo = [s for s in sides if seen is None or (bond, s) not in seen]
-    if not todo:
+    chosen = w.try_bond(bond, todo)
+    if chosen < 0:
         return False
-    ext = w.extents(bond, todo)
-    best = min(range(len(todo)), key=lambda k: (ext[k], k))
-    side, extent = todo[best], ext[best]
-    if extent < baseline or (w.cfg.acceptance == "relaxed" and extent == baseline):
-        if seen is not None:
-            seen.add((bond, side))
-        w.accept(bond, side)
-        return True
-    return False
+    side = todo[chosen]
+    if seen is not None:
+        seen.add((bond, side))
+    w._record(bond, side)
+    return True
 
 
 def _result(w: _Work, before: int) -> UnswapResult:
