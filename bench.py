@@ -218,6 +218,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _phase_seconds(trace):
+    """Host wall time per phase of one contraction, from the trace's
+    cumulative stamps (absorb steps vs unswap calls)."""
+    out = {"absorb": 0.0, "unswap": 0.0}
+    prev = 0.0
+    for t in trace:
+        out[t.phase] = out.get(t.phase, 0.0) + (t.wall_time_s - prev)
+        prev = t.wall_time_s
+    return {k: round(v, 4) for k, v in out.items()}
+
+
 def main():
     args = _args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -360,6 +371,7 @@ def main():
                          "note": "fp64/fp32 CUDA-core Jacobi + GEMM vs the bf16 tensor peak"},
             "profile_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
             "contraction": {"trace_records": len(jobs[-1].trace), "unswap_calls": jobs[-1].unswap_calls,
+                            "phase_s": _phase_seconds(jobs[-1].trace),
                             "accepted_swaps": jobs[-1].accepted_swaps,
                             "max_elements": max(t.elements for t in jobs[-1].trace)},
             "counters": nat.counters(),

@@ -949,21 +949,64 @@ void launch_svd_small(const SvdJob<R>* jobs, int njobs, int max_p, cudaStream_t 
 // block pair per tournament round.
 // ---------------------------------------------------------------------------
 
+// X = A^T or A^H (column-major working copy), V = I, and the per-block
+// partial sums of |X|^2 (grid = kSumBlocks blocks of 256 threads).
 template <typename R>
-__global__ void k_init_large(const cx<R>* __restrict__ A, cx<R>* __restrict__ X,
-                             cx<R>* __restrict__ V, int64_t m, int64_t n) {
+__global__ void __launch_bounds__(256) k_init_large(const cx<R>* __restrict__ A, cx<R>* __restrict__ X,
+                                                    cx<R>* __restrict__ V, int64_t m, int64_t n,
+                                                    double* __restrict__ partial) {
   const int64_t p = m < n ? m : n, q = m < n ? n : m;
-  const int64_t tot = p * q + p * p;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+  const bool tall = m >= n;
+  double acc = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * q;
        e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < p * q) {
-      int64_t j = e / q, i = e % q;
-      X[e] = (m >= n) ? A[i * n + j] : cconj(A[j * n + i]);
-    } else if (V) {
-      int64_t f = e - p * q;
-      int64_t j = f / p, i = f % p;
+    const int64_t j = e / q, i = e - j * q;
+    const cx<R> v = tall ? A[i * n + j] : cconj(A[j * n + i]);
+    X[e] = v;
+    acc += (double)cabs2(v);
+  }
+  if (V)
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < p * p;
+         f += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = f / p, i = f - j * p;
       V[f] = mk<R>(i == j ? 1 : 0, 0);
     }
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// Sorted spectrum (descending, stable rank-by-count) and the truncation rule
+// in one CTA, for p <= 2048 (values staged in shared memory).
+template <typename R>
+__global__ void __launch_bounds__(1024) k_sort_rank(SvdJob<R> J, int64_t p64, int conv, int sweeps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* vals = reinterpret_cast<R*>(smem_raw);
+  R* sorted = vals + p64;
+  const int p = (int)p64;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) vals[c] = J.sig[p + c];
+  __syncthreads();
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    const R v = vals[c];
+    int pos = 0;
+    for (int c2 = 0; c2 < p; ++c2) {
+      const R u = vals[c2];
+      pos += (u > v) || (u == v && c2 < c);
+    }
+    sorted[pos] = v;
+    J.sig[pos] = v;
+    J.perm[pos] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    rank_rule<R>(sorted, p, J.eps, J.chi, &J.info[0], J.disc);
+    J.info[1] = conv ? 0 : 1;
+    J.info[2] = sweeps;
   }
 }
 
@@ -1002,8 +1045,9 @@ __global__ void __launch_bounds__(256) k_jacobi_pair(cx<R>* __restrict__ X, cx<R
 template <typename R, int W2, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
     k_jacobi_pair_cl(cx<R>* __restrict__ X, cx<R>* __restrict__ V, int64_t p, int64_t q, int nb,
-                     int NB, int rnd, int* __restrict__ flag, const double* __restrict__ fro2,
-                     int inner_sweeps, int* __restrict__ open, const int* __restrict__ pairs) {
+                     int NB, int rnd, int* __restrict__ flag, double* __restrict__ fro2,
+                     int inner_sweeps, int* __restrict__ open, const int* __restrict__ pairs,
+                     const double* __restrict__ partials, R* __restrict__ colnorm) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
@@ -1055,13 +1099,43 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
   cluster.sync();
   if (rank == 0) {
     const double tol = rel_tol<R>(q);
-    const double fl = abs_floor<R>(q) * sqrt(*fro2);
+    // the check launch derives ||X||_F^2 from the per-block partial sums
+    // (fixed-order warp reduction: the same value in every CTA) and
+    // publishes it for the rounds that follow
+    __shared__ double f2s;
+    if (check_only) {
+      if (threadIdx.x < 32) {
+        double acc = 0;
+        for (int i = threadIdx.x; i < kSumBlocks; i += 32) acc += partials[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) {
+          f2s = acc;
+          if (blockIdx.x == 0) *fro2 = acc;
+        }
+      }
+      __syncthreads();
+    } else if (threadIdx.x == 0) {
+      f2s = *fro2;
+    }
+    __syncthreads();
+    const double fl = abs_floor<R>(q) * sqrt(f2s);
     bool rot = pair_offdiag<R, W2>(S, tol, fl);
     if (check_only) {
       if (threadIdx.x == 0) {
         if (rot) atomicAdd(flag, 1);
         if (open) open[pidx] = rot ? 1 : 0;
       }
+      // column norms from the Gram diagonal (bitwise the same in every pair
+      // a column belongs to); the last check of a run leaves sigma here
+      if (colnorm)
+        for (int c = threadIdx.x; c < W2; c += blockDim.x) {
+          const int gc = S.col[c];
+          if (gc >= 0) {
+            const double d = (double)S.h[c][c].x;
+            colnorm[gc] = (R)(d > 0 ? sqrt(d) : 0.0);
+          }
+        }
       rot = false;
     }
     if (rot) pair_evd<R, W2>(S, tol, fl, inner_sweeps);
@@ -1357,8 +1431,9 @@ static int env_int(const char* name, int dflt) {
 
 template <typename R, int W2, int CL>
 static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int NB, int rnd,
-                         int* flag_dev, const double* fro2, int inner, cudaStream_t s,
-                         int* open = nullptr, const int* pairs = nullptr, int npairs = 0) {
+                         int* flag_dev, double* fro2, int inner, cudaStream_t s,
+                         int* open = nullptr, const int* pairs = nullptr, int npairs = 0,
+                         const double* partials = nullptr, R* colnorm = nullptr) {
   size_t sm = sizeof(PairSmem<R, W2>);
   static const bool attr = (cudaFuncSetAttribute(k_jacobi_pair_cl<R, W2, CL>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
@@ -1368,7 +1443,7 @@ static void launch_round(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t q, int nb, int
   // rnd == -2: the npairs explicit pairs
   const int np = rnd == -1 ? nb * (nb - 1) / 2 : (rnd == -2 ? npairs : NB / 2);
   k_jacobi_pair_cl<R, W2, CL><<<np * CL, 256, sm, s>>>(Xw, Vw, p, q, nb, NB, rnd, flag_dev, fro2,
-                                                       inner, open, pairs);
+                                                       inner, open, pairs, partials, colnorm);
   MB_LAUNCH_CHECK();
 }
 
@@ -1411,18 +1486,20 @@ int64_t large_pair_capacity(int64_t p) {
 // passes touch only what is still open.
 template <typename R>
 static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const LargeScratch& ws,
-                          cudaStream_t s, int& conv, int& sweeps) {
+                          cudaStream_t s, int& conv, int& sweeps, bool partials_ready,
+                          R* colnorm) {
   static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : (env_int("MB_JACOBI_W2", 32) == 16 ? 16 : 32);
   static const int inner = env_int("MB_JACOBI_INNER", 1);
   static const int debug = env_int("MB_JACOBI_DEBUG", 0);
   static const int dynamic = env_int("MB_JACOBI_DYNAMIC", 1);
   const int w = W2 / 2;
-  // ||Xw||_F^2 (rotation-invariant) for the backward-stability floor
+  // ||Xw||_F^2 (rotation-invariant) for the backward-stability floor: block
+  // partials (from the init kernel, or here), totalled by the check launch
   double* fro2 = ws.red_dev + kSumBlocks;
-  k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(Xw, p * len, ws.red_dev);
-  MB_LAUNCH_CHECK();
-  k_sumsq_final<<<1, 256, 0, s>>>(ws.red_dev, kSumBlocks, fro2);
-  MB_LAUNCH_CHECK();
+  if (!partials_ready) {
+    k_sumsq_partial<R><<<kSumBlocks, 256, 0, s>>>(Xw, p * len, ws.red_dev);
+    MB_LAUNCH_CHECK();
+  }
   const int nb = (int)cdiv(p, w);
   const int NB = nb + (nb & 1);
   const int npair = nb * (nb - 1) / 2;
@@ -1431,15 +1508,17 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const La
   conv = 0;
   sweeps = 0;
   auto round = [&](int rnd, int* open, const int* pairs, int n) {
+    const double* pt = rnd == -1 ? ws.red_dev : nullptr;
+    R* cn = rnd == -1 ? colnorm : nullptr;
     if (W2 == 64) {
-      if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
-      else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+      if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
+      else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
     } else if (W2 == 16) {
-      if (wide) launch_round<R, 16, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
-      else launch_round<R, 16, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+      if (wide) launch_round<R, 16, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
+      else launch_round<R, 16, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
     } else {
-      if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
-      else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n);
+      if (wide) launch_round<R, 32, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
+      else launch_round<R, 32, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
     }
   };
   std::vector<int> pa, pb, used(nb);
@@ -1536,18 +1615,16 @@ void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   PhaseLog plog(s);
   if (J.A) {
-    int blocks = (int)std::min<int64_t>(cdiv(p * q + p * p, 256), 148 * 32);
-    k_init_large<R><<<blocks, 256, 0, s>>>(J.A, J.X, precond ? nullptr : J.V, J.m, J.n);
+    k_init_large<R><<<kSumBlocks, 256, 0, s>>>(J.A, J.X, precond ? nullptr : J.V, J.m, J.n,
+                                               ws.red_dev);
     MB_LAUNCH_CHECK();
   }
   plog.mark("init");
   int conv = 0, sweeps = 0;
   if (!precond) {
-    jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps);
+    // the final check launch leaves the column norms in sig[p, 2p)
+    jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps, J.A != nullptr, J.sig + p);
     plog.mark(sweeps ? "sweeps" : "check");
-    k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(J.X, p, q, J.sig + p);
-    MB_LAUNCH_CHECK();
-    plog.mark("colnorms");
   } else {
     // 1. X0 = Q R (Householder, in the workspace copy)
     cx<R>* Xq = J.W;
@@ -1599,14 +1676,12 @@ void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
         }
       }
     }
-    jacobi_sweeps<R>(Z, nullptr, p, p, ws, s, conv, sweeps);
+    jacobi_sweeps<R>(Z, nullptr, p, p, ws, s, conv, sweeps, false, J.sig + p);
     if (dbg) {
       int bz = count_bad<R>(Z, p * p, s);
       if (bz) fprintf(stderr, "[svd_large dbg] after Jacobi: Z=%d sweeps=%d\n", bz, sweeps);
     }
-    // 3. sigma = column norms of Z J; U~ = Z J / sigma ; U*sigma = X0 U~
-    k_colnorms<R><<<(int)std::min<int64_t>(p, 148 * 8), 256, 0, s>>>(Z, p, p, J.sig + p);
-    MB_LAUNCH_CHECK();
+    // 3. sigma = column norms of Z J (left by the final check); U~ = Z J / sigma ; U*sigma = X0 U~
     if (J.V) {
       int blocks = (int)std::min<int64_t>(cdiv(p * p, 256), 148 * 16);
       k_scale_cols<R><<<blocks, 256, 0, s>>>(Z, J.sig + p, p, J.V);
@@ -1620,18 +1695,24 @@ void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
       }
     }
   }
-  k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
-  MB_LAUNCH_CHECK();
-  plog.mark("sort");
-  {
+  if (p <= 2048) {
+    static const bool attr = (cudaFuncSetAttribute(k_sort_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024),
+                              true);
+    (void)attr;
+    k_sort_rank<R><<<1, 1024, 2 * p * sizeof(R), s>>>(J, p, conv, sweeps + 1);
+    MB_LAUNCH_CHECK();
+  } else {
+    k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
+    MB_LAUNCH_CHECK();
     const size_t sm = (size_t)p * sizeof(R);
     static const bool attr =
         (cudaFuncSetAttribute(k_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true);
     (void)attr;
     k_rank<R><<<1, 256, sm, s>>>(J, p, conv, sweeps + 1);
+    MB_LAUNCH_CHECK();
   }
-  plog.mark("rank");
-  MB_LAUNCH_CHECK();
+  plog.mark("sort+rank");
 }
 
 // QR-step outputs. Q (q x p col-major) / R (upper triangle of the QR'd X).
