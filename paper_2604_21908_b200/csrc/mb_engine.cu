@@ -18,6 +18,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -552,6 +553,8 @@ static SweepPack<R> sweep_pack(int d) {
   pk.info = (int64_t*)E.sw_info->p;
   pk.disc = (double*)E.sw_disc->p;
   pk.tprof = nullptr;
+  static const int tiny = getenv("MB_TINY_WARP") ? atoi(getenv("MB_TINY_WARP")) : 1;
+  pk.tiny = tiny;
   return pk;
 }
 
@@ -569,7 +572,7 @@ static void sweep_launch(SweepPack<R>& pk, int64_t max_pq, int64_t max_pp) {
     cudaEventCreate(&t0);
     cudaEventCreate(&t1);
     cudaEventRecord(t0, E.stream);
-    static thread_local Buf tp = alloc(sizeof(long long) * 4 * kSweepMax);
+    static thread_local Buf tp = alloc(sizeof(long long) * 8 * kSweepMax);
     pk.tprof = (long long*)tp->p;
   }
   {
@@ -585,12 +588,14 @@ static void sweep_launch(SweepPack<R>& pk, int64_t max_pq, int64_t max_pp) {
     fprintf(log, "%d %d %lld %lld %.1f\n", pk.st[0].kind, pk.n, (long long)max_pq, (long long)max_pp,
             ms * 1000.0);
     if (pk.tprof) {  // per step: l r body emit gemm (cycles)
-      long long h[4 * kSweepMax];
-      cudaMemcpy(h, pk.tprof, sizeof(long long) * 4 * pk.n, cudaMemcpyDeviceToHost);
+      long long h[8 * kSweepMax];
+      cudaMemcpy(h, pk.tprof, sizeof(long long) * 8 * kSweepMax, cudaMemcpyDeviceToHost);
+      const long long* g = h + 4 * kSweepMax;
       for (int t = 0; t < pk.n; ++t)
-        fprintf(log, "S %d %lld %lld %lld %lld %lld\n", pk.st[t].kind, (long long)pk.st[t].l,
+        fprintf(log, "S %d %lld %lld %lld %lld %lld %lld %lld %lld\n", pk.st[t].kind, (long long)pk.st[t].l,
                 (long long)pk.st[t].r, h[4 * t + 1] - h[4 * t], h[4 * t + 2] - h[4 * t + 1],
-                h[4 * t + 3] - h[4 * t + 2]);
+                h[4 * t + 3] - h[4 * t + 2], g[4 * t] - h[4 * t], g[4 * t + 1] - g[4 * t],
+                g[4 * t + 2] - g[4 * t + 1]);
     }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
@@ -1294,12 +1299,26 @@ static void init_context(int device) {
 template <typename R>
 static void trial(mb_chain& c, int ng, const int* kinds, const int* qubits, const double* mats,
                   int side, double eps, int64_t chi) {
+  static FILE* log = getenv("MB_TRIAL_LOG") ? fopen(getenv("MB_TRIAL_LOG"), "w") : nullptr;
+  static std::mutex log_mu;
+  auto t0 = std::chrono::steady_clock::now();
+  int n2 = 0;
   for (int t = 0; t < ng; ++t) {
     if (kinds[t] == 1) absorb_1q<R>(c, qubits[t], mats + 32 * t, side);
-    else if (kinds[t] == 2) absorb_2q<R>(c, qubits[t], mats + 32 * t, side, eps, chi);
+    else if (kinds[t] == 2) absorb_2q<R>(c, qubits[t], mats + 32 * t, side, eps, chi), ++n2;
     else throw MbError(MB_ERR_ARG, "gate kind must be 1 or 2");
   }
+  auto t1 = std::chrono::steady_clock::now();
   compress<R>(c, eps, chi);
+  if (log) {  // debug: host wall time of the layer absorption and of compress
+    auto t2 = std::chrono::steady_clock::now();
+    int64_t mx = 0;
+    for (auto& st : c.s) mx = std::max(mx, std::max(st.l, st.r));
+    std::lock_guard<std::mutex> g(log_mu);
+    fprintf(log, "%d %d %lld %.1f %.1f\n", side, n2, (long long)mx,
+            std::chrono::duration<double, std::micro>(t1 - t0).count(),
+            std::chrono::duration<double, std::micro>(t2 - t1).count());
+  }
 }
 
 // Both trials of one adaptive step at once: `l` on the main context (this

@@ -747,6 +747,274 @@ __device__ int64_t sweep_split(unsigned char* smem_raw, const SweepPack<R>& pk, 
   return k;
 }
 
+// ---- warp-level split for tiny steps (p <= 8, q <= 64) -----------------------
+// One warp, no block barriers: lane r holds rows r and r+32 of X (p <= 8
+// columns) and row r of V; Gram entries by fixed-order butterfly reductions;
+// the 8x8 two-sided Jacobi EVD runs in shared memory under __syncwarp; the
+// same convergence rule, sweep cap, sort and truncation rule as the CTA path.
+constexpr int kTinyP = 8, kTinyQ = 64;
+
+template <typename R>
+struct TinySmem {
+  cx<R> xs[kTinyP][kTinyQ + 1];  // X columns (staged for the Gram)
+  cx<R> g[kTinyP][kTinyP + 1];
+  cx<R> w[kTinyP][kTinyP + 1];
+  R cs[kTinyP / 2], sn[kTinyP / 2];
+  cx<R> ph[kTinyP / 2];
+  int pj[kTinyP / 2], pk[kTinyP / 2];
+  R sv[kTinyP];
+  int pv[kTinyP];
+  int64_t rank;
+};
+
+template <typename R>
+__device__ __forceinline__ R warp_sum(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Returns the kept rank (k = p for push steps); called by all 32 lanes of warp 0.
+template <typename R>
+__device__ int64_t warp_split(TinySmem<R>& T, const SweepPack<R>& pk, int s, const SweepStep<R>& st,
+                              const cx<R>* __restrict__ A, int m, int n) {
+  const int lane = threadIdx.x & 31;
+  const bool right = st.kind == kSweepRight;
+  const bool tall = m >= n;
+  const int p = tall ? n : m, q = tall ? m : n;
+  int64_t* info = pk.info + 3 * s;
+  cx<R> x[2][kTinyP], v[kTinyP];
+  double f2 = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = lane + 32 * h;
+#pragma unroll
+    for (int j = 0; j < kTinyP; ++j) {
+      cx<R> e = mk<R>(0, 0);
+      if (r < q && j < p) e = tall ? A[r * n + j] : cconj(A[j * n + r]);
+      x[h][j] = e;
+      f2 += (double)cabs2(e);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kTinyP; ++j) v[j] = mk<R>(lane == j ? 1 : 0, 0);
+  f2 = warp_sum<double>(f2);
+  if (pk.tprof && lane == 0) pk.tprof[4 * kSweepMax + 4 * s + 0] = clock64();
+  const double tol = rel_tol<R>(q), fl = abs_floor<R>(q) * sqrt(f2);
+  const double t2 = tol * tol, fl2 = fl * fl;
+  const int np = p + (p & 1), npairs = np / 2;
+  int it = 0, converged = 0;
+  for (;; ++it) {
+    // Gram via shared memory: stage the columns, lane e computes entry
+    // (j, k) = (e / 8, e % 8), j <= k, over all q rows; mirrored
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < kTinyP; ++j) T.xs[j][lane + 32 * h] = x[h][j];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h, j = e / kTinyP, k = e % kTinyP;
+      if (j <= k && k < p) {
+        cx<R> a = mk<R>(0, 0);
+        for (int r = 0; r < q; ++r) cfmac(a, T.xs[j][r], T.xs[k][r]);
+        T.g[j][k] = a;
+        if (j != k) T.g[k][j] = cconj(a);
+      }
+    }
+    __syncwarp();
+    // any pair above tolerance?
+    bool open = false;
+    if (lane < kTinyP * kTinyP) {
+      const int j = lane / kTinyP, k = lane % kTinyP;
+      if (j < k && k < p) {
+        const double a = T.g[j][j].x, b = T.g[k][k].x, g2 = (double)cabs2(T.g[j][k]);
+        open = a > 0 && b > 0 && g2 > t2 * a * b && g2 > fl2 * (a > b ? a : b);
+      }
+    }
+    // (p <= 8: 28 pairs, lanes 0..31 cover j*8+k < 64 only partly; second half)
+    if (!open && lane + 32 < kTinyP * kTinyP) {
+      const int e = lane + 32, j = e / kTinyP, k = e % kTinyP;
+      if (j < k && k < p) {
+        const double a = T.g[j][j].x, b = T.g[k][k].x, g2 = (double)cabs2(T.g[j][k]);
+        open = a > 0 && b > 0 && g2 > t2 * a * b && g2 > fl2 * (a > b ? a : b);
+      }
+    }
+    const bool any = __any_sync(0xffffffffu, open);
+    if (pk.tprof && lane == 0 && it == 0) pk.tprof[4 * kSweepMax + 4 * s + 1] = clock64();
+    if (!any || it >= 16) {
+      converged = !any;
+      break;
+    }
+    // two-sided Jacobi EVD of the p x p Gram, W accumulated (tournament rounds)
+#pragma unroll
+    for (int e = lane; e < kTinyP * kTinyP; e += 32) T.w[e / kTinyP][e % kTinyP] = mk<R>(e / kTinyP == e % kTinyP ? 1 : 0, 0);
+    __syncwarp();
+    for (int sweep = 0; sweep < kSmallEvdSweeps; ++sweep) {
+      bool rot_any = false;
+      for (int rnd = 0; rnd < np - 1; ++rnd) {
+        bool rot = false;
+        if (lane < npairs) {
+          int j, k;
+          tournament(np, rnd, lane, j, k);
+          if (j > k) { const int t = j; j = k; k = t; }
+          T.pj[lane] = j;
+          T.pk[lane] = k;
+          R c = 1, sn_ = 0;
+          cx<R> ph = mk<R>(1, 0);
+          if (k < p) {
+            const double a = T.g[j][j].x, b = T.g[k][k].x;
+            const cx<R> g = T.g[j][k];
+            const double ga2 = (double)cabs2(g);
+            if (a > 0 && b > 0 && ga2 > t2 * a * b && ga2 > fl2 * (a > b ? a : b)) {
+              const double inv_ga = rsqrt(ga2);
+              const double zeta = 0.5 * (b - a) * inv_ga;
+              const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              const double cc = rsqrt(fma(t, t, 1.0));
+              c = (R)cc;
+              sn_ = (R)(cc * t);
+              ph = mk<R>((R)(g.x * inv_ga), (R)(-g.y * inv_ga));
+              rot = true;
+            }
+          }
+          T.cs[lane] = c;
+          T.sn[lane] = sn_;
+          T.ph[lane] = ph;
+        }
+        rot_any |= __any_sync(0xffffffffu, rot);
+        __syncwarp();
+        // npairs^2 2x2 blocks of g (<= 16) and np*npairs rows of w (<= 32)
+        if (lane < npairs * npairs) {
+          const int pa = lane / npairs, pb = lane % npairs;
+          const R ca = T.cs[pa], sa = T.sn[pa], cb = T.cs[pb], sb = T.sn[pb];
+          if (sa != 0 || sb != 0) {
+            const int ja = T.pj[pa], ka = T.pk[pa], jb = T.pj[pb], kb = T.pk[pb];
+            const cx<R> eac = cconj(T.ph[pa]), eb = T.ph[pb];
+            const cx<R> b00 = T.g[ja][jb], b01 = T.g[ja][kb], b10 = T.g[ka][jb], b11 = T.g[ka][kb];
+            const cx<R> e10 = cmul(eac, b10), e11 = cmul(eac, b11);
+            const cx<R> t00 = csub(cscale(b00, ca), cscale(e10, sa));
+            const cx<R> t01 = csub(cscale(b01, ca), cscale(e11, sa));
+            const cx<R> t10 = cadd(cscale(b00, sa), cscale(e10, ca));
+            const cx<R> t11 = cadd(cscale(b01, sa), cscale(e11, ca));
+            const cx<R> f01 = cmul(t01, eb), f11 = cmul(t11, eb);
+            T.g[ja][jb] = csub(cscale(t00, cb), cscale(f01, sb));
+            T.g[ja][kb] = cadd(cscale(t00, sb), cscale(f01, cb));
+            T.g[ka][jb] = csub(cscale(t10, cb), cscale(f11, sb));
+            T.g[ka][kb] = cadd(cscale(t10, sb), cscale(f11, cb));
+          }
+        }
+        {
+          const int rr = lane / npairs, pb = lane % npairs;  // np * npairs <= 32
+          if (rr < np) {
+            const R cb = T.cs[pb], sb = T.sn[pb];
+            if (sb != 0) {
+              const int jb = T.pj[pb], kb = T.pk[pb];
+              const cx<R> mj = T.w[rr][jb], mk_ = cmul(T.w[rr][kb], T.ph[pb]);
+              T.w[rr][jb] = csub(cscale(mj, cb), cscale(mk_, sb));
+              T.w[rr][kb] = cadd(cscale(mj, sb), cscale(mk_, cb));
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (!rot_any) break;
+    }
+    // X <- X W, V <- V W (each lane its rows)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      cx<R> y[kTinyP];
+#pragma unroll
+      for (int k = 0; k < kTinyP; ++k) {
+        cx<R> a = mk<R>(0, 0);
+#pragma unroll
+        for (int j = 0; j < kTinyP; ++j) cfma(a, x[h][j], T.w[j][k]);
+        y[k] = a;
+      }
+#pragma unroll
+      for (int k = 0; k < kTinyP; ++k) x[h][k] = y[k];
+    }
+    {
+      cx<R> y[kTinyP];
+#pragma unroll
+      for (int k = 0; k < kTinyP; ++k) {
+        cx<R> a = mk<R>(0, 0);
+#pragma unroll
+        for (int j = 0; j < kTinyP; ++j) cfma(a, v[j], T.w[j][k]);
+        y[k] = a;
+      }
+#pragma unroll
+      for (int k = 0; k < kTinyP; ++k) v[k] = y[k];
+    }
+    __syncwarp();
+  }
+  // sigma from the Gram diagonal, rank-by-count sort, truncation rule
+  if (pk.tprof && lane == 0) pk.tprof[4 * kSweepMax + 4 * s + 2] = clock64();
+  if (lane < p) {
+    const R d = T.g[lane][lane].x;
+    const R sg = d > 0 ? sqrt(d) : (R)0;
+    int pos = 0;
+    for (int c2 = 0; c2 < p; ++c2) {
+      const R d2 = T.g[c2][c2].x;
+      const R u = d2 > 0 ? sqrt(d2) : (R)0;
+      pos += (u > sg) || (u == sg && c2 < lane);
+    }
+    T.sv[pos] = sg;
+    T.pv[pos] = lane;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int64_t rk;
+    double disc;
+    rank_rule<R>(T.sv, p, st.kind == kSweepTrunc ? st.eps : 0.0,
+                 st.kind == kSweepTrunc ? st.chi : (int64_t)1 << 62, &rk, &disc);
+    if (st.kind != kSweepTrunc) rk = p;
+    T.rank = rk;
+    info[0] = rk;
+    info[1] = converged ? 0 : 1;
+    info[2] = it;
+    pk.disc[s] = disc;
+  }
+  __syncwarp();
+  if (pk.tprof && lane == 0) pk.tprof[4 * s + 1] = clock64();
+  const int k = (int)T.rank;
+  // emit (as k_emit): U-part m x k, V-part k x n; this lane owns X rows
+  // lane, lane+32 and V row lane
+  cx<R>* Uo = right ? st.nA : pk.carry;
+  cx<R>* Vo = right ? pk.carry : st.nA;
+  const bool su = !right, sv = right;
+  for (int kk = 0; kk < k; ++kk) {
+    const int src = T.pv[kk];
+    const R sg = T.sv[kk];
+    const R inv = sg > 0 ? (R)1 / sg : (R)0;
+    // value of column src from this lane's registers (unrolled select)
+    cx<R> xs0 = mk<R>(0, 0), xs1 = mk<R>(0, 0), vs = mk<R>(0, 0);
+#pragma unroll
+    for (int j = 0; j < kTinyP; ++j)
+      if (j == src) {
+        xs0 = x[0][j];
+        xs1 = x[1][j];
+        vs = v[j];
+      }
+    if (tall) {
+      // U[i][kk] = X(i, src) (/ sigma unless su), rows i = lane, lane+32 < m
+      const cx<R> u0 = su ? xs0 : cscale(xs0, inv), u1 = su ? xs1 : cscale(xs1, inv);
+      if (lane < m) Uo[lane * k + kk] = u0;
+      if (lane + 32 < m) Uo[(lane + 32) * k + kk] = u1;
+      // V-part[kk][c] = conj(V(c, src)) (* sigma if sv), c = lane < n = p
+      if (lane < n) Vo[kk * n + lane] = sv ? cscale(cconj(vs), sg) : cconj(vs);
+    } else {
+      // U[i][kk] = V(i, src) (* sigma if su), i = lane < m = p
+      if (lane < m) Uo[lane * k + kk] = su ? cscale(vs, sg) : vs;
+      // V-part[kk][c] = conj(X(c, src)) (/ sigma unless sv), c = lane, lane+32 < n
+      const cx<R> w0 = sv ? cconj(xs0) : cscale(cconj(xs0), inv);
+      const cx<R> w1 = sv ? cconj(xs1) : cscale(cconj(xs1), inv);
+      if (lane < n) Vo[kk * n + lane] = w0;
+      if (lane + 32 < n) Vo[kk * n + lane + 32] = w1;
+    }
+  }
+  return k;
+}
+
 template <typename R, int NT>
 __global__ void __launch_bounds__(NT) k_sweep(const SweepPack<R> pk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -774,6 +1042,22 @@ __global__ void __launch_bounds__(NT) k_sweep(const SweepPack<R> pk) {
       cta_gemm<R>(st.nB, n, st.B, m, A, n, st.bl * d, n, m);
       if (threadIdx.x == 0) { info[0] = n; info[1] = 0; info[2] = -1; }
       kprev = n;
+    } else if (pk.tiny && (m < n ? m : n) <= kTinyP && (m < n ? n : m) <= kTinyQ) {
+      // tiny step: warp 0 factors and emits, then the block forms the carry product
+      TinySmem<R>& T = *reinterpret_cast<TinySmem<R>*>(smem_raw);
+      __shared__ int64_t k_sh;
+      if (threadIdx.x < 32) {
+        const int64_t k = warp_split<R>(T, pk, s, st, A, (int)m, (int)n);
+        if (threadIdx.x == 0) k_sh = k;
+      }
+      __syncthreads();
+      if (pk.tprof && threadIdx.x == 0) pk.tprof[4 * s + 2] = clock64();
+      const int64_t k = k_sh;
+      if (right)  // next = (sigma V^H) (k x n) @ B (n x d*br)
+        cta_gemm<R>(st.nB, d * st.br, pk.carry, n, st.B, d * st.br, k, d * st.br, n);
+      else        // prev = P (bl*d x m) @ (U sigma) (m x k)
+        cta_gemm<R>(st.nB, k, st.B, m, pk.carry, k, st.bl * d, k, m);
+      kprev = k;
     } else {
       const int64_t p = m < n ? m : n;
       if (p <= 16) kprev = sweep_split<R, 16>(smem_raw, pk, s, st, A, m, n);

@@ -95,6 +95,7 @@ struct SweepPack {
   int64_t* info;  // 3 per step: [0] kept rank, [1] not converged, [2] iterations
   double* disc;   // per step
   long long* tprof;  // debug: 4 clock64 stamps per step, or null
+  int tiny;          // use the warp-level split for p <= 8, q <= 64 steps
 };
 
 template <typename R>
