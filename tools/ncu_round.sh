@@ -11,6 +11,6 @@ timeout 600 $CMD > gpurun_out/bench_${TAG}.jsonl 2> gpurun_out/bench_${TAG}.err
 echo "bench_rc=$?"
 timeout 600 python bench.py --impl reference --steps 1 --warmup 3 > gpurun_out/bench_ref_${TAG}.jsonl 2> gpurun_out/bench_ref_${TAG}.err
 echo "ref_rc=$?"
-timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 60000 --csv \
+timeout 2000 ncu --metrics gpu__time_duration.sum --clock-control none -c 46000 --csv \
     --log-file gpurun_out/launches_${TAG}.csv $CMD --no-cpu-baseline > gpurun_out/ncu_launches_${TAG}.log 2>&1
 echo "launches_rc=$?"
