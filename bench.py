@@ -218,6 +218,20 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+_CLASS_KERNEL = {"svd_small": "k_sweep", "svd_large": "k_jacobi_pair_cl", "gemm": "k_gemm"}
+
+
+def _traffic(cls):
+    """DRAM bytes per launch of the class's dominant kernel, from the committed
+    ncu --set full capture (profiles/r01_kernel_traffic.json), else None."""
+    p = ROOT / "profiles" / "r01_kernel_traffic.json"
+    try:
+        k = json.loads(p.read_text())["kernels"].get(_CLASS_KERNEL.get(cls, ""))
+    except (OSError, ValueError, KeyError):
+        return None
+    return None if k is None else {"kernel": _CLASS_KERNEL[cls], "dram_bytes_per_launch": k["mean"]}
+
+
 def _phase_seconds(trace):
     """Host wall time per phase of one contraction, from the trace's
     cumulative stamps (absorb steps vs unswap calls)."""
@@ -366,7 +380,7 @@ def main():
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved_tf,
                          "peak": bf16, "unit": "TFLOP/s", "frac": achieved_tf / bf16,
-                         "traffic": None, "peak_source": src,
+                         "traffic": _traffic(dom), "peak_source": src,
                          "share_of_device_time": d["ms"] / tot_ms if tot_ms else None,
                          "note": "fp64/fp32 CUDA-core Jacobi + GEMM vs the bf16 tensor peak"},
             "profile_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
