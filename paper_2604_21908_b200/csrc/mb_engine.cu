@@ -170,6 +170,9 @@ struct mb_chain {
   std::vector<Site> s;
   double log_norm = 0.0;
   int center = -1;
+  // true when the engine itself put the chain in mixed canonical form around
+  // `center` (sites left of it left-orthonormal); false for host-built chains
+  bool canonical = false;
 };
 
 namespace mb {
@@ -684,6 +687,7 @@ static void move_center(mb_chain& c, int target) {
     push_left_range<R>(c, c.center, target);
   }
   c.center = target;
+  c.canonical = true;
 }
 
 // ---- two-site operations ------------------------------------------------------
@@ -726,6 +730,8 @@ static void resplit(mb_chain& c, int b, cx<R>* th, int64_t l, int64_t r, double 
   if (!ok) dump_matrix<R>("theta", th, 4 * l, 4 * r);
   c.s[b] = nA;
   c.s[b + 1] = nB;
+  // the split keeps the mixed canonical form only if the center was on the pair
+  c.canonical = c.canonical && (c.center == b || c.center == b + 1);
   c.center = b + 1;
 }
 
@@ -1052,7 +1058,10 @@ static void truncate_sweep(mb_chain& c, double eps, int64_t chi) {
 
 template <typename R>
 static void compress(mb_chain& c, double eps, int64_t chi) {
-  push_right_range<R>(c, 0, c.n - 1);
+  // The orthogonalization sweep (chains.py:274-275) starts at the center when
+  // the engine established the canonical form: the sites left of it are
+  // left-orthonormal already, their QR steps are the identity up to gauge.
+  push_right_range<R>(c, c.canonical && c.center > 0 ? c.center : 0, c.n - 1);
   truncate_sweep<R>(c, eps, chi);
   Site A = c.s[0];
   double f = norm_of<R>(P<R>(A), A.l * c.d * A.r);
@@ -1060,6 +1069,7 @@ static void compress(mb_chain& c, double eps, int64_t chi) {
   scale_site0<R>(c, f);
   c.log_norm += std::log(f);
   c.center = 0;
+  c.canonical = true;
 }
 
 template <typename R>
