@@ -805,20 +805,51 @@ static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, in
   require(c.d == 4, "swap on a non-operator chain");
   require(b >= 0 && b + 1 < c.n, "bond out of range");
   require(ns >= 0 && ns <= 3, "0..3 sides");
+  static FILE* tlog = getenv("MB_TRYBOND_LOG") ? fopen(getenv("MB_TRYBOND_LOG"), "w") : nullptr;
+  double tm[4] = {0, 0, 0, 0};
+  auto tick = std::chrono::steady_clock::now();
+  auto mark = [&](int i) {  // debug: host wall per phase (synchronizing)
+    if (!tlog) return;
+    cudaStreamSynchronize(E.stream);
+    auto now = std::chrono::steady_clock::now();
+    tm[i] = std::chrono::duration<double, std::micro>(now - tick).count();
+    tick = now;
+  };
   move_center<R>(c, b);
-  int64_t l, r;
-  cx<R>* th0 = blob<R>(c, b, 0, l, r);
+  mark(0);
+  const Site A = c.s[b], B = c.s[b + 1];
+  const int64_t l = A.l, r = B.r, chi_b = A.r;
   const int64_t M = 4 * l, N = 4 * r;
   g_tag = 3;
   SvdJob<R> jobs[4];
-  jobs[0] = make_job<R>(0, th0, M, N, eps, chi, true);
+  // Baseline: theta = A B with B right-orthonormal (the center is on A), so
+  // SVD(theta) = SVD(A) (I, B): the baseline factors the 4l x chi site A
+  // instead of the 4l x 4r blob whenever chi < 4r (rank-deficient blobs are
+  // where one-sided Jacobi converges slowest). Same singular values, same
+  // kept rank; the V^H factor is V_A^H B.
+  const bool factor = c.canonical && chi_b < N;
+  if (factor) {
+    jobs[0] = make_job<R>(0, P<R>(A), M, chi_b, eps, chi, true);
+  } else {
+    int64_t l2, r2;
+    cx<R>* th0 = blob<R>(c, b, 0, l2, r2);
+    jobs[0] = make_job<R>(0, th0, M, N, eps, chi, true);
+  }
   run_jobs<R>(&jobs[0], 1);
+  mark(1);
   Gate4<R> sw = swap_gate<R>();
   for (int k = 0; k < ns; ++k) {
     const int sd = sides[k];
     require(sd >= 0 && sd <= 2, "bad side");
     cx<R>* th = (cx<R>*)grow(E.theta[k + 1], (size_t)(M * N) * sizeof(cx<R>));
-    {
+    if (factor) {  // theta_k = (U_k S_k V_A,k^H) B
+      cx<R>* tk = (cx<R>*)grow(E.carry, (size_t)(M * chi_b) * sizeof(cx<R>));
+      {
+        ProfScope ps(P_GEMM, gemm_flops(M, chi_b, std::min(M, chi_b)));
+        launch_trunc_blob<R>(jobs[0], tk, E.stream);
+      }
+      gemm<R>(false, M, N, chi_b, tk, chi_b, P<R>(B), N, th, N);
+    } else {
       ProfScope ps(P_GEMM, gemm_flops(M, N, std::min(M, N)));
       launch_trunc_blob<R>(jobs[0], th, E.stream);
     }
@@ -831,6 +862,7 @@ static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, in
     jobs[k + 1] = make_job<R>(k + 1, th, M, N, eps, chi, true);
   }
   if (ns) run_jobs<R>(jobs + 1, ns);
+  mark(2);
   read_info(ns + 1);
   *baseline = E.h_info[0];
   int best = -1;
@@ -842,10 +874,20 @@ static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, in
   const SvdJob<R>& j = take ? jobs[best + 1] : jobs[0];
   const int64_t k = take ? extents[best] : *baseline;
   Site nA = new_site<R>(l, 4, k), nB = new_site<R>(k, 4, r);
-  emit<R>(j, k, P<R>(nA), false, P<R>(nB), true);
+  if (!take && factor) {  // site b = U_k; site b+1 = (S_k V_A,k^H) B
+    cx<R>* sv = (cx<R>*)grow(E.carry, (size_t)(k * chi_b) * sizeof(cx<R>));
+    emit<R>(j, k, P<R>(nA), false, sv, true);
+    gemm<R>(false, k, N, chi_b, sv, chi_b, P<R>(B), N, P<R>(nB), N);
+  } else {
+    emit<R>(j, k, P<R>(nA), false, P<R>(nB), true);
+  }
   c.s[b] = nA;
   c.s[b + 1] = nB;
   c.center = b + 1;
+  mark(3);
+  if (tlog)
+    fprintf(tlog, "%d %lld %lld %lld %d %.1f %.1f %.1f %.1f\n", b, (long long)M, (long long)N,
+            (long long)*baseline, take ? 1 : 0, tm[0], tm[1], tm[2], tm[3]);
   return take ? best : -1;
 }
 
