@@ -190,3 +190,21 @@ def test_truncation_rank_matches_oracle(golden, golden_arrays):
         for cut in case["cuts"]:
             assert truncation_rank(s, cut["eps"], cut["chi"]) == cut["rank"]
             assert mo.kept_rank(s, cut["eps"], cut["chi"]) == cut["rank"]
+
+
+def test_trial_layer_encoding():
+    """mb_trial / mb_trial_pair gate arrays: kind, lower site, matrix slot."""
+    from paper_2604_21908_b200.chains import gate_tensor_ordered
+    from paper_2604_21908_b200.circuit import gate_unitary
+    from paper_2604_21908_b200.driver import _encode_layer
+
+    layer = [Gate("h", (3,)), Gate("cx", (5, 4)), Gate("rzz", (1, 2), (0.3,))]
+    kinds, sites, mats = _encode_layer(layer)
+    assert list(kinds) == [1, 2, 2] and list(sites) == [3, 4, 1]
+    np.testing.assert_array_equal(mats[0, :4], gate_unitary(layer[0]).reshape(4))
+    np.testing.assert_array_equal(mats[0, 4:], 0)
+    np.testing.assert_array_equal(mats[1], gate_tensor_ordered(layer[1]).reshape(16))
+    with pytest.raises(ValueError):
+        _encode_layer([Gate("cx", (0, 2))])
+    k0, s0, m0 = _encode_layer([])
+    assert len(k0) == 1 and m0.shape == (1, 16)
