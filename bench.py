@@ -75,7 +75,7 @@ def _workload(name, dtype):
     return {"workload": f"{n}q peaked circuit, middle-MPO contraction + peak extraction",
             "config": name, "qubits": n, "depth_budget": depth, "obfuscation_swaps": obf,
             "seed": seed, "epsilon": 2e-3, "chi_max": 8192, "tau": 1_000_000,
-            "side_mode": "adaptive", "unswap": "parity-parallel/strict", "dtype": dtype,
+            "side_mode": "adaptive", "dtype": dtype,
             "l2": "working set re-created every step (fresh MPO per contraction)"}
 
 
@@ -163,10 +163,23 @@ def cpu_reference(name, steps):
     from oracle import mirror_oracle as mo
 
     n, gates = _oracle_circuit(name)
+    # every host thread (torchrun sets OMP_NUM_THREADS=1 for its ranks);
+    # report what the BLAS pool actually runs with
+    threads = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+
+        ctx = threadpool_limits(limits=threads, user_api="blas")
+        info = [p for p in threadpool_info() if p.get("user_api") == "blas"]
+        if info:
+            threads = int(info[0].get("num_threads", threads))
+    except ImportError:  # pragma: no cover - threadpoolctl is in the image
+        ctx = None
     t0 = time.perf_counter()
     res = mo.contract(n, gates, mo.OConfig(), max_steps=steps)
     spent = time.perf_counter() - t0
-    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    if ctx is not None:
+        ctx.restore_original_limits()
     return {"seconds": spent, "absorb_steps": steps, "source_gates": res.consumed_source,
             "value": res.consumed_source / spent if spent > 0 else 0.0, "threads": threads,
             "complete": res.state is not None}
