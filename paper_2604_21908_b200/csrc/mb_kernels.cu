@@ -394,18 +394,29 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
   __syncthreads();
   const double t2 = tol * tol, f2 = floor_abs * floor_abs;
   const int npairs = np / 2;
-  // This thread's work items of every round, decoded once: (pa, pb) 2x2 blocks
-  // of h, then (row, pb) pairs of w. (Integer division by the runtime pair
-  // count inside the round loop was ~20% of the EVD's issue slots.)
-  constexpr int kItems = (3 * W2 * W2 / 4 + NT - 1) / NT;  // NT = blockDim.x
-  const int nblk = npairs * npairs, nitems = nblk + np * npairs;
+  // This thread's work items of every round, decoded once: the 2x2 blocks
+  // (pa <= pb) of the upper block triangle of h (h stays exactly Hermitian:
+  // each off-diagonal block is written with its conjugate transpose), then the
+  // (row, pb) pairs of w. (Integer division by the runtime pair count inside
+  // the round loop was ~20% of the EVD's issue slots.)
+  constexpr int kItems = ((W2 / 2) * (W2 / 2 + 1) / 2 + W2 * W2 / 2 + NT - 1) / NT;  // NT = blockDim.x
+  const int nblk = npairs * (npairs + 1) / 2, nitems = nblk + np * npairs;
   int code[kItems];
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     const int e = tid + k * NT;
-    if (e < nblk) code[k] = (e / npairs) | ((e % npairs) << 8);
-    else if (e < nitems) code[k] = ((e - nblk) / npairs) | (((e - nblk) % npairs) << 8) | (1 << 16);
-    else code[k] = -1;
+    if (e < nblk) {
+      int pa = 0, f = e;  // row-wise enumeration of pa <= pb
+      while (f >= npairs - pa) {
+        f -= npairs - pa;
+        ++pa;
+      }
+      code[k] = pa | ((pa + f) << 8);
+    } else if (e < nitems) {
+      code[k] = ((e - nblk) / npairs) | (((e - nblk) % npairs) << 8) | (1 << 16);
+    } else {
+      code[k] = -1;
+    }
   }
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) S.flag = 0;
@@ -459,10 +470,20 @@ __device__ int pair_evd(PairSmem<R, W2>& S, double tol, double floor_abs, int ma
           cx<R> t11 = cadd(cscale(b01, sa), cscale(e11, ca));
           // B' = T J_b : cols (j,k)
           cx<R> f01 = cmul(t01, eb), f11 = cmul(t11, eb);
-          S.h[ja][jb] = csub(cscale(t00, cb), cscale(f01, sb));
-          S.h[ja][kb] = cadd(cscale(t00, sb), cscale(f01, cb));
-          S.h[ka][jb] = csub(cscale(t10, cb), cscale(f11, sb));
-          S.h[ka][kb] = cadd(cscale(t10, sb), cscale(f11, cb));
+          const cx<R> n00 = csub(cscale(t00, cb), cscale(f01, sb));
+          const cx<R> n01 = cadd(cscale(t00, sb), cscale(f01, cb));
+          const cx<R> n10 = csub(cscale(t10, cb), cscale(f11, sb));
+          const cx<R> n11 = cadd(cscale(t10, sb), cscale(f11, cb));
+          S.h[ja][jb] = n00;
+          S.h[ja][kb] = n01;
+          S.h[ka][jb] = n10;
+          S.h[ka][kb] = n11;
+          if (pa != pb) {  // mirrored block B'_ba = (B'_ab)^H
+            S.h[jb][ja] = cconj(n00);
+            S.h[kb][ja] = cconj(n01);
+            S.h[jb][ka] = cconj(n10);
+            S.h[kb][ka] = cconj(n11);
+          }
         } else {
           const int rr = cd & 255, pb = (cd >> 8) & 255;
           const R cb = S.cs[pb], sb = S.sn[pb];
