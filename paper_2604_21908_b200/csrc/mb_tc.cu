@@ -14,10 +14,13 @@
 // Shared-memory operand layout: the canonical K-major SWIZZLE_NONE
 // ("interleaved") UMMA layout — 8-row x 16-byte core matrices, row blocks
 // SBO = 128 B apart, the two 16-byte K chunks of one MMA LBO = 2048 B apart.
+#include <cuda.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "mb_kernels.cuh"
 
@@ -185,6 +188,159 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                  "r"(TC_N * TC_NACC));
 }
 
+// ---- TMA-fed, warp-specialized variant ----------------------------------------
+// Operand tiles arrive by cp.async.bulk.tensor (one 4-D box per operand and
+// stage) straight into the canonical K-major SWIZZLE_NONE core-matrix layout:
+// the global row-major (rows x K) operand is viewed as the 4-D tensor
+// (c%4, r%8, r/8, c/4) with byte strides (4, ld*4, 8*ld*4, 16), so a
+// {4, 8, 16, 8} box lands as (c/4)*2048 + (r/8)*128 + (r%8)*16 + (c%4)*4
+// bytes — LBO = 2048, SBO = 128. Warp 0 lane 0 produces (full barriers with
+// expect_tx), warp 1 lane 0 issues the MMAs and releases each stage with
+// tcgen05.commit onto its empty barrier; all four warps drain TMEM.
+constexpr int TMA_STAGES = 6;
+constexpr uint32_t TMA_TILE_BYTES = TC_M * TC_K * 4;  // 16 KB per operand per stage
+
+struct __align__(1024) TmaSmem {
+  float a[TMA_STAGES][TC_M * TC_K];
+  float b[TMA_STAGES][TC_N * TC_K];
+  uint64_t full[TMA_STAGES];
+  uint64_t empty[TMA_STAGES];
+  uint64_t done;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_tc_gemm_tma(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                  float* __restrict__ C, int64_t ldc, int64_t K) {
+  extern __shared__ __align__(1024) unsigned char tma_raw[];
+  TmaSmem& S = *reinterpret_cast<TmaSmem*>(tma_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * TC_M, n0 = (int64_t)blockIdx.x * TC_N;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&S.tmem_base)),
+                 "r"(TC_N * TC_NACC));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < TMA_STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], 1);
+    }
+    mbar_init(&S.done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = S.tmem_base;
+  const int nk = (int)(K / TC_K);
+  if (warp == 0 && lane == 0) {  // producer
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % TMA_STAGES;
+      if (kt >= TMA_STAGES) mbar_wait(&S.empty[s], (uint32_t)((kt / TMA_STAGES - 1) & 1));
+      mbar_expect_tx(&S.full[s], 2 * TMA_TILE_BYTES);
+      tma_load_4d(&S.a[s][0], &ta, 0, 0, (int)(m0 / 8), kt * (TC_K / 4), &S.full[s]);
+      tma_load_4d(&S.b[s][0], &tb, 0, 0, (int)(n0 / 8), kt * (TC_K / 4), &S.full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    const uint32_t idesc = tc_idesc();
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % TMA_STAGES;
+      mbar_wait(&S.full[s], (uint32_t)((kt / TMA_STAGES) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t abase = smem_u32(&S.a[s][0]), bbase = smem_u32(&S.b[s][0]);
+      const uint32_t dacc = tmem + (uint32_t)((kt % TC_NACC) * TC_N);
+#pragma unroll
+      for (int k8 = 0; k8 < TC_K / 8; ++k8) {
+        const uint32_t off = (uint32_t)(2 * k8) * TC_LBO;
+        umma_tf32(dacc, umma_desc(abase + off), umma_desc(bbase + off), idesc,
+                  (kt >= TC_NACC || k8 > 0) ? 1u : 0u);
+      }
+      umma_commit(&S.empty[s]);  // stage free once these MMAs have read it
+    }
+    umma_commit(&S.done);
+  }
+  __syncwarp();
+  mbar_wait(&S.done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int64_t row = m0 + warp * 32 + lane;
+  float* crow = C + row * ldc + n0;
+  const int nacc = nk < TC_NACC ? nk : TC_NACC;
+#pragma unroll 1
+  for (int j = 0; j < TC_N / 8; ++j) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int a = 0; a < nacc; ++a) {
+      uint32_t v[8];
+      const uint32_t taddr =
+          tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(a * TC_N + j * 8);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] += __uint_as_float(v[t]);
+    }
+    *reinterpret_cast<float4*>(crow + j * 8) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(crow + j * 8 + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TC_N * TC_NACC));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 4-D view (c%4, r%8, r/8, c/4) of a row-major (rows x cols) fp32 operand
+static bool make_operand_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {4, 8, (cuuint64_t)(rows / 8), (cuuint64_t)(cols / 4)};
+  const cuuint64_t strides[3] = {(cuuint64_t)cols * 4, (cuuint64_t)cols * 4 * 8, 16};
+  const cuuint32_t box[4] = {4, 8, TC_M / 8, TC_K / 4};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---- operand preparation (3xTF32 split of the real embedding) -------------
 
 __device__ __forceinline__ float tf32_hi(float x) {
@@ -264,12 +420,22 @@ void tc_gemm_c64(int64_t M, int64_t N, int64_t K, const cx<float>* A, int64_t ld
       A, lda, M, K, A3, Mp, K3);
   k_tc_prep_b<<<(int)std::min<int64_t>((Np * K3 + thr - 1) / thr, 148 * 32), thr, 0, s>>>(
       B, ldb, K, N, B3, Np, K3);
-  static const bool attr = (cudaFuncSetAttribute(k_tc_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sizeof(TcSmem)),
-                            true);
-  (void)attr;
   dim3 grid((unsigned)(Np / TC_N), (unsigned)(Mp / TC_M));
-  k_tc_gemm_tf32<<<grid, TC_THREADS, sizeof(TcSmem), s>>>(A3, K3, B3, K3, Cp, Np, K3);
+  static const bool use_tma = !getenv("MB_TC_TMA") || atoi(getenv("MB_TC_TMA")) != 0;
+  CUtensorMap ta, tb;
+  if (use_tma && make_operand_map(&ta, A3, Mp, K3) && make_operand_map(&tb, B3, Np, K3)) {
+    static const bool attr2 = (cudaFuncSetAttribute(k_tc_gemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)sizeof(TmaSmem)),
+                               true);
+    (void)attr2;
+    k_tc_gemm_tma<<<grid, TC_THREADS, sizeof(TmaSmem), s>>>(ta, tb, Cp, Np, K3);
+  } else {
+    static const bool attr = (cudaFuncSetAttribute(k_tc_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)sizeof(TcSmem)),
+                              true);
+    (void)attr;
+    k_tc_gemm_tf32<<<grid, TC_THREADS, sizeof(TcSmem), s>>>(A3, K3, B3, K3, Cp, Np, K3);
+  }
   k_tc_unpad<<<(int)std::min<int64_t>((M * N + thr - 1) / thr, 148 * 32), thr, 0, s>>>(Cp, Np, M, N,
                                                                                           C, ldc);
   g_launches.fetch_add(4, std::memory_order_relaxed);
