@@ -425,3 +425,20 @@ def test_concurrent_trials_match_sequential(golden, name):
     assert [(t.phase, t.unitaries_consumed, t.elements) for t in seq.trace] == \
         [(t.phase, t.unitaries_consumed, t.elements) for t in par.trace]
     np.testing.assert_array_equal(dense_output(seq), dense_output(par))
+
+
+def test_c36_prefix_trace_matches_oracle():
+    """Large-scale parity: the first 160 absorption steps of the bench's 36q
+    instance (7 unswap calls, MPO up to 7M elements, bonds up to 1024) take
+    exactly the oracle's decisions (tests/golden/make_c36_prefix.py)."""
+    import json
+    from pathlib import Path
+
+    from bench import _instance
+    from paper_2604_21908_b200 import Contraction
+
+    ref = json.loads((Path(__file__).resolve().parent / "golden" / "c36_prefix160_trace.json").read_text())
+    job = Contraction(_instance("c36").circuit, ContractionConfig())
+    job.advance(max_steps=ref["steps"])
+    got = [[t.phase, t.unitaries_consumed, t.elements] for t in job.trace]
+    assert got == ref["trace"]
