@@ -1315,32 +1315,6 @@ __global__ void __launch_bounds__(1024) k_sort_rank(SvdJob<R> J, int64_t p64, in
   }
 }
 
-template <typename R, int W2>
-__global__ void __launch_bounds__(256) k_jacobi_pair(cx<R>* __restrict__ X, cx<R>* __restrict__ V,
-                                                     int64_t p, int64_t q, int nb, int NB, int rnd,
-                                                     int* __restrict__ flag,
-                                                     const double* __restrict__ fro2,
-                                                     int inner_sweeps) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
-  constexpr int w = W2 / 2;
-  int a, b;
-  tournament(NB, rnd, blockIdx.x, a, b);
-  for (int c = threadIdx.x; c < W2; c += blockDim.x) {
-    int blk = c < w ? a : b;
-    int64_t gc = (int64_t)blk * w + (c % w);
-    S.col[c] = (blk < nb && gc < p) ? (int)gc : -1;
-  }
-  __syncthreads();
-  const double tol = rel_tol<R>(q);
-  const double fl = abs_floor<R>(q) * sqrt(*fro2);
-  pair_gram<R, W2>(S, X, q);
-  if (!pair_offdiag<R, W2>(S, tol, fl)) return;
-  pair_evd<R, W2>(S, tol, fl, inner_sweeps);
-  pair_apply<R, W2>(S, X, q);
-  if (V) pair_apply<R, W2>(S, V, p);
-  if (threadIdx.x == 0) atomicOr(flag, 1);
-}
 
 // Cluster variant: the CL CTAs of a cluster share one block pair. Each CTA
 // forms the partial Gram of its slice of rows; the partials are summed
@@ -1464,22 +1438,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
   }
 }
 
-template <typename R>
-__global__ void k_colnorms(const cx<R>* __restrict__ X, int64_t p, int64_t q, R* __restrict__ out) {
-  __shared__ double red[256];
-  for (int64_t j = blockIdx.x; j < p; j += gridDim.x) {
-    double acc = 0;
-    for (int64_t i = threadIdx.x; i < q; i += blockDim.x) acc += (double)cabs2(X[j * q + i]);
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[j] = (R)sqrt(red[0]);
-    __syncthreads();
-  }
-}
 
 template <typename R>
 __global__ void k_sort_desc(const R* __restrict__ vals, int64_t p, R* __restrict__ sig,
