@@ -1,13 +1,21 @@
 // CUDA kernels of the B200 middle-MPO engine (sm_100a).
 //
-//  * k_gemm          : tiled complex GEMM (pair blob, R-carry, L-carry).
-//  * k_gate2/k_gate1 : 4x4 / 2x2 gate application on blob / site legs
-//                      (reference chains.py:190-216).
-//  * k_svd_small     : whole-matrix one-CTA block Jacobi SVD with in-kernel
-//                      sort and truncation rank (tensor.py:84-136) — batched.
-//  * k_jacobi_pair   : one block-pair step of the multi-CTA block Jacobi SVD.
-//  * k_emit          : writes truncated factors straight into site layout.
-//  * k_peak          : single-CTA sequential MPS marginal sweep.
+//  * k_gemm            : tiled complex GEMM (pair blob, carries).
+//  * k_gate2/k_gate1   : 4x4 / 2x2 gate application on blob / site legs
+//                        (reference chains.py:190-216).
+//  * k_svd_small       : whole-matrix one-CTA Gram + Jacobi-EVD SVD with
+//                        in-kernel sort and truncation rank (tensor.py:84-136),
+//                        batched; k_svd_small_cl splits tall inputs over a
+//                        thread-block cluster (DSMEM Gram reduction).
+//  * k_sweep           : device-resident run of canonical-form steps (SVD split,
+//                        factors into the new sites, carry into the neighbour,
+//                        ranks kept on the device); warp-level tiny path.
+//  * k_jacobi_pair_cl  : block one-sided Jacobi for p > 64 on thread-block
+//                        clusters: tournament rounds, all-pairs checks, and
+//                        explicit open-pair rounds (dynamic ordering).
+//  * k_trunc_blob      : truncated product U_k S_k V_k^H with device-side k.
+//  * k_emit            : writes truncated factors straight into site layout.
+//  * k_peak            : single-CTA sequential MPS marginal sweep.
 #include "mb_kernels.cuh"
 
 #include <cooperative_groups.h>
