@@ -1775,12 +1775,21 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const La
   const int NB = nb + (nb & 1);
   const int npair = nb * (nb - 1) / 2;
   // 8-CTA clusters when the pairs alone cannot fill the chip
-  const bool wide = (NB / 2) * 4 < 148 && len >= 8 * 64;
+  // 8-CTA clusters only when a launch's pairs alone cannot fill the chip
+  // (MB_JACOBI_WIDE: 0 never, 1 per launch (default), 2 per matrix)
+  static const int wide_mode = env_int("MB_JACOBI_WIDE", 1);
+  const bool tall = len >= 8 * 64;
+  auto use8 = [&](int pairs_in_launch) {
+    if (!tall || wide_mode == 0) return false;
+    if (wide_mode == 2) return (NB / 2) * 4 < 148;
+    return pairs_in_launch * 4 < 148;
+  };
   conv = 0;
   sweeps = 0;
   auto round = [&](int rnd, int* open, const int* pairs, int n) {
     const double* pt = rnd == -1 ? ws.red_dev : nullptr;
     R* cn = rnd == -1 ? colnorm : nullptr;
+    const bool wide = use8(rnd == -1 ? npair : (rnd == -2 ? n : NB / 2));
     if (W2 == 64) {
       if (wide) launch_round<R, 64, 8>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
       else launch_round<R, 64, 4>(Xw, Vw, p, len, nb, NB, rnd, ws.flag_dev, fro2, inner, s, open, pairs, n, pt, cn);
