@@ -51,63 +51,69 @@ long long launch_count() { return g_launches.load(); }
 
 constexpr int GBM = 64, GBN = 64, GBK = 16;
 
-template <typename R, bool CT>
+// BT x BT output tile per 256-thread CTA (16 x 16 threads, BT/16 x BT/16
+// outputs each): BT = 64 normally, 32 when the 64-tile grid cannot fill the
+// 148 SMs (the 256^3 - 1024 x 256^2 blob products of the contraction).
+template <typename R, bool CT, int BT>
 __global__ void __launch_bounds__(256) k_gemm(int64_t M, int64_t N, int64_t K,
                                               const cx<R>* __restrict__ A, int64_t lda,
                                               const cx<R>* __restrict__ B, int64_t ldb,
                                               cx<R>* __restrict__ C, int64_t ldc) {
-  __shared__ cx<R> As[GBK][GBM + 1];
-  __shared__ cx<R> Bs[GBK][GBN + 1];
+  constexpr int TM = BT / 16;
+  __shared__ cx<R> As[GBK][BT + 1];
+  __shared__ cx<R> Bs[GBK][BT + 1];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t m0 = (int64_t)blockIdx.y * GBM, n0 = (int64_t)blockIdx.x * GBN;
-  cx<R> acc[4][4];
+  const int64_t m0 = (int64_t)blockIdx.y * BT, n0 = (int64_t)blockIdx.x * BT;
+  cx<R> acc[TM][TM];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = mk<R>(0, 0);
+    for (int j = 0; j < TM; ++j) acc[i][j] = mk<R>(0, 0);
   const cx<R> zero = mk<R>(0, 0);
   for (int64_t k0 = 0; k0 < K; k0 += GBK) {
 #pragma unroll
-    for (int t = 0; t < (GBM * GBK) / 256; ++t) {
+    for (int t = 0; t < (BT * GBK + 255) / 256; ++t) {
       int e = tid + 256 * t;
+      if (e >= BT * GBK) break;
       if (!CT) {
         int mm = e / GBK, kk = e % GBK;
         int64_t gm = m0 + mm, gk = k0 + kk;
         As[kk][mm] = (gm < M && gk < K) ? A[gm * lda + gk] : zero;
       } else {
-        int kk = e / GBM, mm = e % GBM;
+        int kk = e / BT, mm = e % BT;
         int64_t gm = m0 + mm, gk = k0 + kk;
         As[kk][mm] = (gm < M && gk < K) ? cconj(A[gk * lda + gm]) : zero;
       }
     }
 #pragma unroll
-    for (int t = 0; t < (GBN * GBK) / 256; ++t) {
+    for (int t = 0; t < (BT * GBK + 255) / 256; ++t) {
       int e = tid + 256 * t;
-      int kk = e / GBN, nn = e % GBN;
+      if (e >= BT * GBK) break;
+      int kk = e / BT, nn = e % BT;
       int64_t gk = k0 + kk, gn = n0 + nn;
       Bs[kk][nn] = (gk < K && gn < N) ? B[gk * ldb + gn] : zero;
     }
     __syncthreads();
 #pragma unroll 4
     for (int kk = 0; kk < GBK; ++kk) {
-      cx<R> a[4], b[4];
+      cx<R> a[TM], b[TM];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < TM; ++j) b[j] = Bs[kk][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cfma(acc[i][j], a[i], b[j]);
+        for (int j = 0; j < TM; ++j) cfma(acc[i][j], a[i], b[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < TM; ++i) {
     int64_t gm = m0 + ty + 16 * i;
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TM; ++j) {
       int64_t gn = n0 + tx + 16 * j;
       if (gn < N) C[gm * ldc + gn] = acc[i][j];
     }
@@ -118,11 +124,21 @@ template <typename R>
 void launch_gemm(bool conjTransA, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64_t lda,
                  const cx<R>* B, int64_t ldb, cx<R>* C, int64_t ldc, cudaStream_t s) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid((unsigned)cdiv(N, GBN), (unsigned)cdiv(M, GBM));
-  if (conjTransA)
-    k_gemm<R, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
-  else
-    k_gemm<R, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  static const int small_tiles = getenv("MB_GEMM_T32") ? atoi(getenv("MB_GEMM_T32")) : 1;
+  const bool t32 = small_tiles && cdiv(N, GBN) * cdiv(M, GBM) < 148 && K >= 64;
+  if (t32) {
+    dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32));
+    if (conjTransA)
+      k_gemm<R, true, 32><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+    else
+      k_gemm<R, false, 32><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  } else {
+    dim3 grid((unsigned)cdiv(N, GBN), (unsigned)cdiv(M, GBM));
+    if (conjTransA)
+      k_gemm<R, true, 64><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+    else
+      k_gemm<R, false, 64><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  }
   MB_LAUNCH_CHECK();
 }
 
