@@ -613,7 +613,7 @@ __device__ void job_init(const SvdJob<R>& J, int64_t p64, int64_t q64) {
 // directions at the Gram's rounding level only churn (seen on contraction
 // blobs: 30-sweep runs). The outer loop recomputes a fresh Gram of the rotated
 // columns, which resolves what is left.
-constexpr int kSmallEvdSweeps = 6;
+constexpr int kSmallEvdSweeps = 4;
 
 template <typename R>
 struct JobPack {
