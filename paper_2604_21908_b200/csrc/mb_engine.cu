@@ -520,8 +520,12 @@ static bool sweep_enabled() {
   static const bool on = !getenv("MB_SWEEP") || atoi(getenv("MB_SWEEP")) != 0;
   return on;
 }
-constexpr int64_t kSweepGemmMax = (int64_t)1 << 18;  // complex MACs of a fused carry product
-constexpr int64_t kSweepSvdMax = (int64_t)1 << 20;   // p*p*q of a fused factorization
+// complex MACs of a fused carry product / p*p*q of a fused factorization
+// (log2 overridable with MB_SWEEP_GEMM_LOG2 / MB_SWEEP_SVD_LOG2)
+static const int64_t kSweepGemmMax =
+    (int64_t)1 << (getenv("MB_SWEEP_GEMM_LOG2") ? atoi(getenv("MB_SWEEP_GEMM_LOG2")) : 16);
+static const int64_t kSweepSvdMax =
+    (int64_t)1 << (getenv("MB_SWEEP_SVD_LOG2") ? atoi(getenv("MB_SWEEP_SVD_LOG2")) : 17);
 
 static bool fuse_svd(int64_t m, int64_t n) {
   const int64_t p = std::min(m, n), q = std::max(m, n);
