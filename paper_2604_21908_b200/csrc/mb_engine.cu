@@ -825,6 +825,53 @@ static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, in
   const int64_t l = A.l, r = B.r, chi_b = A.r;
   const int64_t M = 4 * l, N = 4 * r;
   g_tag = 3;
+  // small blobs: the whole step in one CTA launch (k_try_bond_small)
+  static const bool fused_ok = !getenv("MB_TRYBOND_FUSED") || atoi(getenv("MB_TRYBOND_FUSED")) != 0;
+  const int64_t pb = std::min(M, N), qb = std::max(M, N);
+  if (fused_ok && ns <= 1 && pb <= kSmallP && pb * pb * qb <= kSweepSvdMax &&
+      M * N * chi_b <= kSweepGemmMax) {
+    TryBondArgs<R> a;
+    a.A = P<R>(A);
+    a.B = P<R>(B);
+    a.l = l;
+    a.chi_b = chi_b;
+    a.r = r;
+    a.side = ns ? sides[0] : -1;
+    require(a.side >= -1 && a.side <= 2, "bad side");
+    a.relaxed = relaxed ? 1 : 0;
+    a.eps = eps;
+    a.chi = chi;
+    Site nA = new_site<R>(l, 4, pb), nB = new_site<R>(pb, 4, r);
+    a.nA = P<R>(nA);
+    a.nB = P<R>(nB);
+    a.scratch = (cx<R>*)grow(E.theta[1], (size_t)(4 * M * N) * sizeof(cx<R>));
+    a.X = (cx<R>*)grow(E.X[0], (size_t)(pb * qb) * sizeof(cx<R>));
+    a.V = (cx<R>*)grow(E.V[0], (size_t)(pb * pb) * sizeof(cx<R>));
+    a.sig = (R*)grow(E.sig[0], 2 * kSmallP * sizeof(R));
+    a.perm = (int*)grow(E.perm[0], kSmallP * sizeof(int));
+    a.info = reinterpret_cast<int64_t*>(E.d_info->p);
+    a.disc = reinterpret_cast<double*>(E.d_disc->p);
+    {
+      ProfScope ps(P_SVD_SMALL, 16.0 * pb * pb * qb);
+      launch_try_bond_small<R>(a, E.stream);
+    }
+    E.counters[0] += 1 + ns;
+    d2h(E.h_info, E.d_info->p, sizeof(int64_t) * 6);
+    sync();
+    *baseline = E.h_info[0];
+    if (E.h_info[1]) E.counters[4]++;
+    if (ns) {
+      extents[0] = E.h_info[3];
+      if (E.h_info[4]) E.counters[4]++;
+    }
+    const bool take = ns && E.h_info[5] != 0;
+    const int64_t k = take ? extents[0] : *baseline;
+    c.s[b] = Site{nA.b, l, k};
+    c.s[b + 1] = Site{nB.b, k, r};
+    c.center = b + 1;
+    mark(3);
+    return take ? 0 : -1;
+  }
   SvdJob<R> jobs[4];
   // Baseline: theta = A B with B right-orthonormal (the center is on A), so
   // SVD(theta) = SVD(A) (I, B): the baseline factors the 4l x chi site A

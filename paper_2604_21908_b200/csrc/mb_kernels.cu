@@ -1115,6 +1115,130 @@ __global__ void __launch_bounds__(NT) k_sweep(const SweepPack<R> pk) {
   }
 }
 
+// ---- one unswap bond step in one CTA (small blobs) -----------------------------
+// SVD + emission of a small M x N matrix by the whole CTA (W2 >= min(M, N)):
+// U-part (M x k) into Uo, V-part (k x N) into Vo with k_emit's scaling flags.
+template <typename R, int W2>
+__device__ int64_t cta_split(unsigned char* smem_raw, const cx<R>* A, int64_t m, int64_t n, double eps,
+                             int64_t chi, const TryBondArgs<R>& a, int64_t* info, double* disc,
+                             cx<R>* Uo, bool su, cx<R>* Vo, bool sv) {
+  PairSmem<R, W2>& S = *reinterpret_cast<PairSmem<R, W2>*>(smem_raw);
+  SvdJob<R> J;
+  J.A = A;
+  J.X = a.X;
+  J.V = a.V;
+  J.sig = a.sig;
+  J.perm = a.perm;
+  J.m = m;
+  J.n = n;
+  J.eps = eps;
+  J.chi = chi;
+  J.info = info;
+  J.disc = disc;
+  J.W = nullptr;
+  small_svd_body<R, W2, 512>(S, J);
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  const bool tall = m >= n;
+  const int k = (int)S.rank, ni = (int)n;
+  for (int e = threadIdx.x; e < (int)(m * k + k * n); e += blockDim.x) {
+    if (e < m * k) {
+      const int i = e / k, kk = e % k;
+      const int src = S.pv[kk];
+      const R sg = S.sv[kk];
+      cx<R> v;
+      if (tall) {
+        v = J.X[(int64_t)src * q + i];
+        if (!su) v = sg > 0 ? cscale(v, (R)1 / sg) : mk<R>(0, 0);
+      } else {
+        v = J.V[(int64_t)src * p + i];
+        if (su) v = cscale(v, sg);
+      }
+      Uo[e] = v;
+    } else {
+      const int f = e - (int)(m * k), kk = f / ni, c = f % ni;
+      const int src = S.pv[kk];
+      const R sg = S.sv[kk];
+      cx<R> v;
+      if (tall) {
+        v = cconj(J.V[(int64_t)src * p + c]);
+        if (sv) v = cscale(v, sg);
+      } else {
+        v = cconj(J.X[(int64_t)src * q + c]);
+        if (!sv) v = sg > 0 ? cscale(v, (R)1 / sg) : mk<R>(0, 0);
+      }
+      Vo[f] = v;
+    }
+  }
+  __syncthreads();
+  return k;
+}
+
+template <typename R>
+__device__ int64_t cta_split_any(unsigned char* smem_raw, const cx<R>* A, int64_t m, int64_t n,
+                                 double eps, int64_t chi, const TryBondArgs<R>& a, int64_t* info,
+                                 double* disc, cx<R>* Uo, bool su, cx<R>* Vo, bool sv) {
+  const int64_t p = m < n ? m : n;
+  if (p <= 16) return cta_split<R, 16>(smem_raw, A, m, n, eps, chi, a, info, disc, Uo, su, Vo, sv);
+  if (p <= 32) return cta_split<R, 32>(smem_raw, A, m, n, eps, chi, a, info, disc, Uo, su, Vo, sv);
+  return cta_split<R, 64>(smem_raw, A, m, n, eps, chi, a, info, disc, Uo, su, Vo, sv);
+}
+
+// unswap.py:137-167 for one candidate side, in one launch: blob = A B, the
+// normalized split (baseline rank k0, factors into the output sites), the
+// truncated blob, the SWAP as an index permutation of its (t1,b1)/(t2,b2)
+// legs, the candidate split (rank k1, factors into scratch), the acceptance
+// rule, and the accepted factors copied over the baseline ones.
+// info: [k0, notconv0, it0, k1, notconv1, accepted]
+template <typename R>
+__global__ void __launch_bounds__(512) k_try_bond_small(const TryBondArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t M = 4 * a.l, N = 4 * a.r;
+  cx<R>* theta = a.scratch;              // M x N
+  cx<R>* cand = a.scratch + M * N;       // M x N (SWAP-ed blob)
+  cx<R>* uc = a.scratch + 2 * M * N;     // M x k1
+  cx<R>* vc = a.scratch + 3 * M * N;     // k1 x N
+  cta_gemm<R>(theta, N, a.A, a.chi_b, a.B, N, M, N, a.chi_b);
+  __syncthreads();
+  const int64_t k0 = cta_split_any<R>(smem_raw, theta, M, N, a.eps, a.chi, a, a.info, a.disc, a.nA, false,
+                                      a.nB, true);
+  if (a.side < 0) {
+    if (threadIdx.x == 0) { a.info[3] = -1; a.info[4] = 0; a.info[5] = 0; }
+    return;
+  }
+  cta_gemm<R>(theta, N, a.nA, k0, a.nB, N, M, N, k0);  // theta_k0 = U_k0 (S V^H)_k0
+  __syncthreads();
+  const bool top = a.side == 0 || a.side == 2, bottom = a.side == 1 || a.side == 2;
+  const int r = (int)a.r, n = (int)N;
+  for (int e = threadIdx.x; e < (int)(M * N); e += blockDim.x) {
+    const int row = e / n, col = e - row * n;
+    int l = row >> 2, t1 = (row >> 1) & 1, b1 = row & 1;
+    int t2 = col / (2 * r), b2 = (col / r) & 1, rr = col % r;
+    if (top) { const int t = t1; t1 = t2; t2 = t; }
+    if (bottom) { const int t = b1; b1 = b2; b2 = t; }
+    cand[e] = theta[(int64_t)(l * 4 + t1 * 2 + b1) * N + (t2 * 2 + b2) * r + rr];
+  }
+  __syncthreads();
+  const int64_t k1 = cta_split_any<R>(smem_raw, cand, M, N, a.eps, a.chi, a, a.info + 3, a.disc + 1, uc,
+                                      false, vc, true);
+  const bool take = k1 < k0 || (a.relaxed && k1 == k0);
+  if (take) {
+    for (int64_t e = threadIdx.x; e < M * k1; e += blockDim.x) a.nA[e] = uc[e];
+    for (int64_t e = threadIdx.x; e < k1 * N; e += blockDim.x) a.nB[e] = vc[e];
+  }
+  if (threadIdx.x == 0) a.info[5] = take ? 1 : 0;
+}
+
+template <typename R>
+void launch_try_bond_small(const TryBondArgs<R>& a, cudaStream_t s) {
+  const size_t sm = sizeof(PairSmem<R, kSmallP>);
+  static const bool attr = (cudaFuncSetAttribute(k_try_bond_small<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sm),
+                            true);
+  (void)attr;
+  k_try_bond_small<R><<<1, 512, sm, s>>>(a);
+  MB_LAUNCH_CHECK();
+}
+
 template <typename R>
 void launch_sweep(const SweepPack<R>& pk, cudaStream_t s) {
   const size_t sm = sizeof(PairSmem<R, kSmallP>);
@@ -2418,6 +2542,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
                                   cx<R>*, cudaStream_t);                                        \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
   template void launch_sweep<R>(const SweepPack<R>&, cudaStream_t);                             \
+  template void launch_try_bond_small<R>(const TryBondArgs<R>&, cudaStream_t);                 \
   template void launch_trunc_blob<R>(const SvdJob<R>&, cx<R>*, cudaStream_t);                   \
   template void launch_emit<R>(const SvdJob<R>&, int64_t, cx<R>*, bool, cx<R>*, bool,            \
                                cudaStream_t);                                                   \

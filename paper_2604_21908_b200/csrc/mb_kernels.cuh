@@ -101,6 +101,31 @@ struct SweepPack {
 template <typename R>
 void launch_sweep(const SweepPack<R>& pk, cudaStream_t s);
 
+// One small unswap bond step in one CTA (k_try_bond_small): blob A B, the
+// normalized split into nA / nB (capacity min(4l, 4r)), the SWAP-ed candidate
+// (side 0 top, 1 bottom, 2 both, -1 none) and the acceptance rule.
+template <typename R>
+struct TryBondArgs {
+  const cx<R>* A;  // site b (l x 4 x chi_b)
+  const cx<R>* B;  // site b+1 (chi_b x 4 x r), right-orthonormal
+  int64_t l, chi_b, r;
+  int side, relaxed;
+  double eps;
+  int64_t chi;
+  cx<R>* nA;       // l x 4 x k (capacity k <= min(4l, 4r))
+  cx<R>* nB;       // k x 4 x r
+  cx<R>* scratch;  // 4 * (4l) * (4r)
+  cx<R>* X;        // p * q
+  cx<R>* V;        // p * p
+  R* sig;          // 2 * kSmallP
+  int* perm;       // kSmallP
+  int64_t* info;   // 6: k0, notconv0, it0, k1, notconv1, accepted
+  double* disc;    // 2
+};
+
+template <typename R>
+void launch_try_bond_small(const TryBondArgs<R>& a, cudaStream_t s);
+
 // theta_k = U_k S_k V_k^H of a finished job, k read from job.info[0] on the device
 template <typename R>
 void launch_trunc_blob(const SvdJob<R>& job, cx<R>* out, cudaStream_t s);
