@@ -37,14 +37,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    for src in SOURCES:  # the translation units are independent: compile them concurrently
         obj = OUT.parent / (Path(src).stem + ".o")
         cmd = [_nvcc(), *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
         objs.append(str(obj))
+    for cmd, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     cmd = [_nvcc(), *ARCH, "-shared", "-o", str(OUT), *objs, "-lcudart"]
     subprocess.run(cmd, check=True)
     for o in objs:
