@@ -442,3 +442,22 @@ def test_c36_prefix_trace_matches_oracle():
     job.advance(max_steps=ref["steps"])
     got = [[t.phase, t.unitaries_consumed, t.elements] for t in job.trace]
     assert got == ref["trace"]
+
+
+@pytest.mark.gpu
+def test_c36_fp32_vs_fp64_mpo_fidelity():
+    """configs[2]'s fp32-vs-fp64 check: the first 160 absorption steps of the
+    36q instance (bonds to 256, ~0.9M elements) in complex64 take the same
+    decisions as in complex128, and the two middle MPOs agree to fidelity
+    1 - F <= 1e-5 (the north star's fp32 tolerance; measured ~6e-11,
+    profiles/r01_fp32_fp64_fidelity.jsonl). F is the normalized
+    Hilbert-Schmidt overlap from tools/mpo_fidelity.py."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    from mpo_fidelity import run_pair
+
+    out = run_pair("c36", 160, "cuda")
+    assert out["same_trace"], out
+    assert 1.0 - out["fidelity"] <= 1e-5, out

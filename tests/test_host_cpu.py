@@ -208,3 +208,32 @@ def test_trial_layer_encoding():
         _encode_layer([Gate("cx", (0, 2))])
     k0, s0, m0 = _encode_layer([])
     assert len(k0) == 1 and m0.shape == (1, 16)
+
+
+def test_hs_overlap_transfer_sweep_matches_dense():
+    """tools/mpo_fidelity.py's transfer-matrix overlap (the fp32-vs-fp64
+    fidelity checker) against the dense Hilbert-Schmidt product."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    from mpo_fidelity import hs_overlap
+
+    rng = np.random.default_rng(5)
+
+    def rand_mpo(bonds):
+        return [rng.standard_normal((bonds[i], 2, 2, bonds[i + 1]))
+                + 1j * rng.standard_normal((bonds[i], 2, 2, bonds[i + 1])) for i in range(len(bonds) - 1)]
+
+    def dense(sites):
+        t = sites[0]
+        for s in sites[1:]:
+            t = np.tensordot(t, s, axes=([-1], [0]))
+        return t.reshape(-1)
+
+    a, b = rand_mpo([1, 3, 5, 2, 1]), rand_mpo([1, 2, 4, 3, 1])
+    ref = np.vdot(dense(a), dense(b))
+    lg, ph = hs_overlap(a, b)
+    assert np.isclose(np.exp(lg) * ph, ref, rtol=1e-12)
+    la, _ = hs_overlap(a, a)
+    assert np.isclose(np.exp(la), np.vdot(dense(a), dense(a)).real, rtol=1e-12)

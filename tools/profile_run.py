@@ -1,7 +1,7 @@
 """Profile one contraction on the device: per-kernel-class CUDA-event time,
 engine counters, trace summary. Used for the profiles/ summaries.
 
-    python tools/profile_run.py --config c20 [--dtype complex64] [--max-steps K]
+    python tools/profile_run.py --config c20 [--dtype complex64] [--max-steps K] [--chi X]
 """
 
 from __future__ import annotations
@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--max-steps", type=int, default=None)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--side", default="adaptive")
+    ap.add_argument("--chi", type=int, default=8192)
     a = ap.parse_args()
     inst = _instance(a.config)
     nat.load()
@@ -35,7 +36,7 @@ def main():
     if a.profile:
         nat.profile_begin()
     t0 = time.perf_counter()
-    job = Contraction(inst.circuit, ContractionConfig(dtype=a.dtype, side_mode=a.side))
+    job = Contraction(inst.circuit, ContractionConfig(dtype=a.dtype, side_mode=a.side, chi_max=a.chi))
     last = t0
     done = False
     while not done:
