@@ -116,6 +116,15 @@ int mb_batch_swap_extents(mb_chain* c, int nb, const int* bonds, const int* mine
  * normalized) split with the center at bond+1. */
 int mb_try_bond(mb_chain* c, int bond, int nsides, const int* sides, double eps, int64_t chi_max,
                 int relaxed, int64_t* baseline, int64_t* extents, int* accepted);
+/* A run of single-side mb_try_bond steps over `bonds` in order — one
+ * (side, parity) batch of the reference's parity-parallel unswap cycle
+ * (unswap.py:214-240, the inner `for bond in range(parity, n - 1, 2)` loop)
+ * driven from C++ instead of one host-language call per bond. Same steps,
+ * same order, same results as nb calls of mb_try_bond. Per bond: accepted[i]
+ * (1 = the swap on `side` was taken), was[i] / now[i] = the bond dimension
+ * before / after the step. */
+int mb_try_bond_run(mb_chain* c, int nb, const int* bonds, int side, double eps, int64_t chi_max,
+                    int relaxed, int* accepted, int64_t* was, int64_t* now);
 /* Two-sided sweep: orthogonalize left->right, truncate right->left,
  * renormalize into log_norm; center ends at 0.                 chains.py:262-285 */
 int mb_compress(mb_chain* c, double eps, int64_t chi_max);

@@ -62,6 +62,7 @@ _SIGS = {
     "mb_batch_swap_extents": (_i, [_p, _i, _ip, _ip, _i, _d, _i64, _i64p, _i64p]),
     "mb_compress": (_i, [_p, _d, _i64]),
     "mb_try_bond": (_i, [_p, _i, _i, _ip, _d, _i64, _i, _i64p, _i64p, _ip]),
+    "mb_try_bond_run": (_i, [_p, _i, _ip, _i, _d, _i64, _i, _ip, _i64p, _i64p]),
     "mb_trial": (_i, [_p, _i, _ip, _ip, _dp, _i, _d, _i64]),
     "mb_trial_pair": (_i, [_p, _i, _ip, _ip, _dp, _i, _ip, _ip, _dp, _d, _i64,
                            C.POINTER(_p), C.POINTER(_p)]),

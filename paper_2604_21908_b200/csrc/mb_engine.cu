@@ -1731,6 +1731,27 @@ int mb_try_bond(mb_chain* c, int bond, int nsides, const int* sides, double eps,
   });
 }
 
+int mb_try_bond_run(mb_chain* c, int nb, const int* bonds, int side, double eps, int64_t chi,
+                    int relaxed, int* accepted, int64_t* was, int64_t* now) {
+  MB_TRY({
+    require(eps >= 0 && chi >= 1, "bad truncation parameters");
+    require(nb >= 0 && (nb == 0 || (bonds && accepted && was && now)), "bad run arrays");
+    for (int i = 0; i < nb; ++i) {
+      const int b = bonds[i];
+      require(b >= 0 && b + 1 < c->n, "bond out of range");
+      was[i] = c->s[b].r;
+      int64_t base = 0;
+      int64_t ext[3];
+      int acc;
+      if (c->dtype == MB_C64) acc = try_bond<float>(*c, b, 1, &side, eps, chi, relaxed != 0, &base, ext);
+      else acc = try_bond<double>(*c, b, 1, &side, eps, chi, relaxed != 0, &base, ext);
+      accepted[i] = acc >= 0 ? 1 : 0;
+      now[i] = c->s[b].r;
+    }
+    return 0;
+  });
+}
+
 int mb_compress(mb_chain* c, double eps, int64_t chi) {
   MB_TRY({
     require(eps >= 0 && chi >= 1, "bad truncation parameters");

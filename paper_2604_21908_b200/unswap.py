@@ -12,6 +12,7 @@ candidate is re-split in place with ``mb_pair_swap(recenter=0)``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,6 +24,8 @@ from .sharding import Comm, unswap_parity_batched
 
 _EVALUATION_SLACK = 16
 
+# MB_BOND_RUN=0: drive each bond step of a parity batch from Python instead
+_BOND_RUN = os.environ.get("MB_BOND_RUN", "1") != "0"
 PARALLEL_CYCLE = (("both", 0), ("both", 1), ("left", 0), ("left", 1), ("right", 0), ("right", 1))
 
 
@@ -129,8 +132,23 @@ class _Work:
                                         self.cfg.chi_max, 1), "apply batched candidate")
         self._record(bond, side)
 
-    def _record(self, bond: int, side: str) -> None:
+    def try_bond_run(self, bonds, side: str):
+        """One (side, parity) batch of single-side bond steps in one engine
+        call (mb_try_bond_run): per bond (accepted, dim before, dim after)."""
+        nb = len(bonds)
+        b_arr = (C.c_int * max(1, nb))(*bonds)
+        acc = (C.c_int * max(1, nb))()
+        was = np.zeros(max(1, nb), dtype=np.int64)
+        now = np.zeros(max(1, nb), dtype=np.int64)
+        nat.check(nat._lib.mb_try_bond_run(self.m._h, nb, b_arr, nat.SIDE[side], self.cfg.epsilon,
+                                           self.cfg.chi_max, int(self.cfg.acceptance == "relaxed"),
+                                           acc, nat.i64ptr(was), nat.i64ptr(now)), "try bond run")
         self.refresh()
+        return [bool(acc[i]) for i in range(nb)], was[:nb].tolist(), now[:nb].tolist()
+
+    def _record(self, bond: int, side: str, refresh: bool = True) -> None:
+        if refresh:
+            self.refresh()
         tau = QubitPermutation.transposition(self.n, bond, bond + 1)
         if side in ("left", "both"):
             self.left = self.left.compose(tau)
@@ -216,10 +234,20 @@ def unswap_parallel(m: MatrixProductOperator, cfg: UnswapConfig) -> UnswapResult
     for _ in range(cfg.max_outer_iterations):
         reduced = False
         for side, parity in PARALLEL_CYCLE:
-            for bond in range(parity, n - 1, 2):
-                was = w.bonds[bond]
-                if _try_bond(w, bond, (side,), None) and w.bonds[bond] < was:
-                    reduced = True
+            bonds = list(range(parity, n - 1, 2))
+            if not _BOND_RUN:
+                for bond in bonds:
+                    was = w.bonds[bond]
+                    if _try_bond(w, bond, (side,), None) and w.bonds[bond] < was:
+                        reduced = True
+                continue
+            # the same steps in the same order, driven from C++ (one call)
+            acc, was, now = w.try_bond_run(bonds, side)
+            for bond, a, b0, b1 in zip(bonds, acc, was, now):
+                if a:
+                    w._record(bond, side, refresh=False)
+                    if b1 < b0:
+                        reduced = True
         if not reduced:
             break
     return _result(w, before)
