@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1424,6 +1426,56 @@ static void trial(mb_chain& c, int ng, const int* kinds, const int* qubits, cons
   }
 }
 
+// The auxiliary context's host thread: created once, then handed one job per
+// trial pair (a thread spawn + join per absorption step cost more than the
+// condition-variable handoff). Heap-allocated and never destroyed: the
+// detached thread may still be parked on the condition variable at exit.
+class AuxWorker {
+ public:
+  static AuxWorker& get() {
+    static AuxWorker* w = new AuxWorker();
+    return *w;
+  }
+  void submit(std::function<void()> f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = std::move(f);
+      pending_ = true;
+      done_ = false;
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return done_; });
+  }
+
+ private:
+  AuxWorker() {
+    std::thread([this] {
+      for (;;) {
+        std::function<void()> f;
+        {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return pending_; });
+          f = std::move(job_);
+          pending_ = false;
+        }
+        f();
+        {
+          std::lock_guard<std::mutex> lk(mu_);
+          done_ = true;
+        }
+        cv_.notify_all();
+      }
+    }).detach();
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::function<void()> job_;
+  bool pending_ = false, done_ = false;
+};
+
 // Both trials of one adaptive step at once: `l` on the main context (this
 // thread), `r` on the auxiliary context (a second thread and stream). The
 // two trials share the input chain's site buffers read-only. Afterwards the
@@ -1447,14 +1499,15 @@ static void trial_pair(mb_chain& l, int nl, const int* kl, const int* ql, const 
   }
   Engine& A = g_aux;
   // the input chain's pending producers are on the main stream
-  cudaEvent_t ready_ev;
-  ck(cudaEventCreateWithFlags(&ready_ev, cudaEventDisableTiming), "event");
+  static cudaEvent_t ready_ev = nullptr;  // main-thread only (trial pairs do not nest)
+  if (!ready_ev) ck(cudaEventCreateWithFlags(&ready_ev, cudaEventDisableTiming), "event");
   ck(cudaEventRecord(ready_ev, M.stream), "event record");
   ck(cudaStreamWaitEvent(A.stream, ready_ev, 0), "stream wait");
   A.prof = M.prof;
   std::string aux_err;
   int aux_code = 0;
-  std::thread worker([&] {
+  AuxWorker& worker = AuxWorker::get();
+  worker.submit([&] {
     g_cur = &A;
     try {
       ck(cudaSetDevice(A.device), "cudaSetDevice");
@@ -1464,6 +1517,9 @@ static void trial_pair(mb_chain& l, int nl, const int* kl, const int* ql, const 
       aux_code = e.code;
     } catch (const std::exception& e) {
       aux_err = e.what();
+      aux_code = MB_ERR_ARG;
+    } catch (...) {
+      aux_err = "unknown error in the auxiliary trial";
       aux_code = MB_ERR_ARG;
     }
   });
@@ -1478,9 +1534,8 @@ static void trial_pair(mb_chain& l, int nl, const int* kl, const int* ql, const 
     main_err = e.what();
     main_code = MB_ERR_ARG;
   }
-  worker.join();
+  worker.wait();
   ck(cudaStreamSynchronize(A.stream), "aux sync");
-  cudaEventDestroy(ready_ev);
   for (auto& st : r.s)
     if (st.b && st.b->s == A.stream) st.b->s = M.stream;
   for (int i = 0; i < 8; ++i) {
