@@ -461,3 +461,25 @@ def test_c36_fp32_vs_fp64_mpo_fidelity():
     out = run_pair("c36", 160, "cuda")
     assert out["same_trace"], out
     assert 1.0 - out["fidelity"] <= 1e-5, out
+
+
+@pytest.mark.gpu
+def test_bond_run_matches_per_bond_calls(golden, monkeypatch):
+    """mb_try_bond_run (a parity batch of bond steps driven from C++) takes
+    the same steps as one mb_try_bond call per bond from Python."""
+    import importlib
+
+    us = importlib.import_module("paper_2604_21908_b200.unswap")
+
+    for case in golden["unswap"]:
+        if case["strategy"] != "parity-parallel":
+            continue
+        out = []
+        for flag in (True, False):
+            monkeypatch.setattr(us, "_BOND_RUN", flag)
+            m = _perm_mpo(tuple(case["perm"]), case["side"])
+            res = unswap(m, UnswapConfig(epsilon=1e-10, chi_max=4096, strategy="parity-parallel"))
+            out.append((res.accepted_swaps, res.left_perm.mapping, res.right_perm.mapping,
+                        res.reduced.bond_dims(), mpo_to_dense(res.reduced)))
+        assert out[0][:4] == out[1][:4], case
+        np.testing.assert_array_equal(out[0][4], out[1][4])
