@@ -64,6 +64,12 @@ int mb_profile_end(double* ms_per_class, long long* launches_per_class, double* 
  * [4] svd non-converged, [5] max p seen, [6] host-to-device bytes (incl. gate
  * matrices passed as kernel parameters), [7] device-to-host bytes. */
 int mb_counters(long long* out8);
+/* Per-stage device time of the large-SVD Gram path over the last profiled
+ * region (CUDA events around every launch): stages 0 Gram GEMM, 1 panel
+ * (Householder vectors), 2 Hermitian matrix-vector products, 3 trailing
+ * rank-2k update, 4 divide and conquer, 5 back-transformation, 6 X V and
+ * column norms; with the algorithmic bytes and flops of those launches. */
+int mb_profile_eig(double* ms7, long long* launches7, double* bytes7, double* flops7);
 
 /* ---- construction / inspection --------------------------------------- */
 mb_chain* mb_identity_mpo(int n, int dtype);                          /* chains.py:83-88 */
@@ -167,6 +173,18 @@ int mb_gemm(const double* a, const double* b, int64_t m, int64_t n, int64_t k, i
  * weight. */
 int mb_svd_truncate(const double* a, int64_t m, int64_t n, int dtype, double eps, int64_t chi_max,
                     double* u, double* s, double* v, int64_t* rank, double* discarded);
+
+/* Eigen-decomposition of a host n x n Hermitian complex128 matrix (row-major,
+ * interleaved) on the device by the large-SVD path's eigensolver (Householder
+ * tridiagonalization + divide and conquer + back-transformation, mb_eig.cu).
+ * w: n eigenvalues ascending; v: n x n row-major, column j = eigenvector j.
+ * The Gram eigenproblem behind the truncated SVD of tensor.py:84-116. */
+int mb_herm_eig(const double* a, int64_t n, double* w, double* v);
+/* Test hook: the next n convergence outcomes of the large Jacobi path count
+ * as failures. One failure is absorbed by the perturbed retry; two make the
+ * call fail with MB_ERR_NUMERIC (SvdConvergenceError in Python), like
+ * _svd_with_retry (tensor.py:139-150). */
+int mb_debug_fail_svd(int n);
 
 #ifdef __cplusplus
 }

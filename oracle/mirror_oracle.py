@@ -729,9 +729,11 @@ class OResult:
     consumed_source: int = 0
 
 
-def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None):
+def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None, on_record=None):
     """driver.py:250-346. ``max_steps`` bounds the number of absorption steps
-    (used only by the bounded CPU baseline; None = run to completion)."""
+    (used only by the bounded CPU baseline; None = run to completion).
+    ``on_record(record, chain)`` is called after every trace record (used by
+    the long-run golden generator to stream the trace)."""
     if not gates:
         raise ValueError("circuit has no gates")
     if cfg.tau < 4 * n:
@@ -771,6 +773,8 @@ def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None):
             if any(d >= cfg.chi_max for d in c.bonds()):
                 sat += 1
             trace.append(("absorb", consumed, c.elements()))
+            if on_record is not None:
+                on_record(trace[-1], c)
             if max_steps is not None and step >= max_steps:
                 return OResult(None, pi_out, pi_in, trace, c.elements(), sat, logs, consumed_src)
         if not (left.gates or right.gates):
@@ -782,6 +786,8 @@ def contract(n, gates, cfg: OConfig = OConfig(), max_steps=None):
         c = compress(st.c, cfg.epsilon, cfg.chi_max)
         after = c.elements()
         trace.append(("unswap", consumed, after))
+        if on_record is not None:
+            on_record(trace[-1], c)
         red = (before - after) / before if before else 0.0
         if after >= cfg.tau and red < 0.01:
             stalls.append(red)

@@ -14,7 +14,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libmirrorbreak_b200.so"
-SOURCES = ["mb_kernels.cu", "mb_tc.cu", "mb_engine.cu"]
+SOURCES = ["mb_kernels.cu", "mb_tc.cu", "mb_eig.cu", "mb_engine.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]

@@ -71,6 +71,9 @@ _SIGS = {
     "mb_peak": (_i, [_p, _u8p, _dp]),
     "mb_sample": (_i, [_p, _i64, _dp, _u8p]),
     "mb_svd_truncate": (_i, [_dp, _i64, _i64, _i, _d, _i64, _dp, _dp, _dp, _i64p, _dp]),
+    "mb_herm_eig": (_i, [_dp, _i64, _dp, _dp]),
+    "mb_debug_fail_svd": (_i, [_i]),
+    "mb_profile_eig": (_i, [_dp, _i64p, _dp, _dp]),
     "mb_gemm": (_i, [_dp, _dp, _i64, _i64, _i64, _i, _i, _dp]),
 }
 
@@ -104,9 +107,20 @@ def load(init: bool = True):
     return _lib
 
 
+class SvdConvergenceError(NativeError):
+    """The SVD failed even after a perturbed retry (the reference's
+    tensor.SvdConvergenceError, tensor.py:26)."""
+
+
+ERR_NUMERIC = -3
+
+
 def check(rc: int, what: str) -> None:
     if rc != 0:
-        raise NativeError(f"{what}: {_lib.mb_last_error().decode()}")
+        msg = f"{what}: {_lib.mb_last_error().decode()}"
+        if rc == ERR_NUMERIC and "converge" in msg:
+            raise SvdConvergenceError(msg)
+        raise NativeError(msg)
 
 
 def handle(h, what: str):
@@ -158,6 +172,21 @@ def profile_end() -> dict:
     check(load().mb_profile_end(ms, n, fl), "mb_profile_end")
     return {k: {"ms": ms[i], "launch_groups": int(n[i]), "flops": fl[i]}
             for i, k in enumerate(PROFILE_CLASSES)}
+
+
+EIG_STAGES = ("gram", "trd_panel", "trd_symv", "trd_update", "dc", "backtransform", "xv")
+
+
+def profile_eig() -> dict:
+    """Per-stage device time, launches, algorithmic bytes and flops of the
+    large-SVD Gram path over the last profiled region (mb_profile_eig)."""
+    ms = (C.c_double * 7)()
+    n = (C.c_longlong * 7)()
+    by = (C.c_double * 7)()
+    fl = (C.c_double * 7)()
+    check(load().mb_profile_eig(ms, n, by, fl), "mb_profile_eig")
+    return {k: {"ms": ms[i], "launches": int(n[i]), "bytes": by[i], "flops": fl[i]}
+            for i, k in enumerate(EIG_STAGES)}
 
 
 def stream_handle() -> int:

@@ -11,7 +11,9 @@
 // gauge-invariant).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
+#include <deque>
 #include <condition_variable>
 #include <functional>
 #include <cmath>
@@ -26,6 +28,7 @@
 #include <thread>
 #include <vector>
 
+#include "mb_eig.cuh"
 #include "mb_kernels.cuh"
 #include "mirrorbreak_b200.h"
 
@@ -73,6 +76,8 @@ struct Engine {
   static constexpr int kSlots = 4;
   Buf theta[kSlots], X[kSlots], V[kSlots], sig[kSlots], perm[kSlots], W[kSlots];
   Buf carry, env[2], amp, misc, tcws;
+  // Gram-eigensolver path of the large SVD (mb_eig.cu)
+  Buf eigws;
   // device-resident sweep runs (k_sweep)
   Buf sw_X, sw_V, sw_sig, sw_perm, sw_carry, sw_info, sw_disc;
   int64_t* h_sw_info = nullptr;  // 3 * kSweepMax
@@ -81,10 +86,13 @@ struct Engine {
   int* h_lg = nullptr;
   int64_t h_lg_cap = 0;
   long long counters[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [6] h2d bytes, [7] d2h bytes
-  // profiling
+  // profiling: records pending on the device, harvested lazily into the
+  // per-class totals (bounded event count, no synchronization)
   bool prof = false;
-  std::vector<ProfRec> recs;
+  std::deque<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
+  double pms[6] = {}, pfl[6] = {};
+  long long pn[6] = {};
 };
 
 // Two engine contexts (stream + scratch + readback buffers each): the main
@@ -157,6 +165,23 @@ struct ProfScope {
       cudaEvent_t b = ev_get();
       cudaEventRecord(b, E.stream);
       E.recs.push_back({cls, a, b, flops});
+      if (E.recs.size() > 4096) harvest(E, false);
+    }
+  }
+  // fold completed records (all of them when `all`) into the class totals
+  static void harvest(Engine& e, bool all) {
+    while (!e.recs.empty()) {
+      ProfRec& r = e.recs.front();
+      if (all) cudaEventSynchronize(r.b);
+      else if (cudaEventQuery(r.b) != cudaSuccess) break;
+      float t = 0;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      e.pms[r.cls] += t;
+      e.pn[r.cls] += 1;
+      e.pfl[r.cls] += r.flops;
+      e.pool.push_back(r.a);
+      e.pool.push_back(r.b);
+      e.recs.pop_front();
     }
   }
 };
@@ -309,6 +334,19 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
   }
   for (int i = 0; i < nj; ++i) {
     int64_t p = jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n;
+    if (p > kSmallP && gram_path_ok(p, jobs[i].eps)) {
+      // truncated / values-only: fp64 Gram eigenproblem (mb_eig.cu)
+      const double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m), pd = (double)p;
+      ProfScope ps(P_SVD_LARGE, 8.0 * q * pd * pd * 2.0 + (16.0 / 3.0 + 8.0 + 2.0) * pd * pd * pd);
+      void* ws = grow(E.eigws, eig_workspace_bytes(p));
+      if (!jobs[i].W)  // values-only batch jobs: Y and V in shared scratch
+        jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
+                                 large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
+      svd_gram<R>(jobs[i], ws, E.stream);
+      finish_large<R>(jobs[i], 1, 0, E.stream);
+      E.counters[1]++;
+      continue;
+    }
     if (p > kSmallP) {
       double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
       ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * (double)p * (double)p * q);
@@ -342,14 +380,23 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
   }
 }
 
+// A factorization that did not converge even after the large path's
+// perturbed retry is an error, as in the reference (tensor.py:139-150:
+// one retry on a perturbed copy, then SvdConvergenceError).
+static void nonconverged(long long flag) {
+  if (!flag) return;
+  E.counters[4]++;
+  throw MbError(MB_ERR_NUMERIC, "SVD failed to converge after perturbed retry");
+}
+
 // Read back kept ranks (and discarded weights) of the first `ns` slots.
 static void read_info(int ns) {
   d2h(E.h_info, E.d_info->p, sizeof(int64_t) * 3 * ns);
   d2h(E.h_disc, E.d_disc->p, sizeof(double) * ns);
   sync();
   for (int i = 0; i < ns; ++i) {
-    if (E.h_info[3 * i + 1]) E.counters[4]++;
     E.counters[2] += E.h_info[3 * i + 2];
+    nonconverged(E.h_info[3 * i + 1]);
   }
 }
 
@@ -726,9 +773,6 @@ static void resplit(mb_chain& c, int b, cx<R>* th, int64_t l, int64_t r, double 
   run_jobs<R>(&j, 1);
   read_info(1);
   const int64_t k = E.h_info[0];
-  if (check_sites_enabled() && getenv("MB_DUMP_DIR")) {
-    // keep a copy of theta before the SVD could touch scratch
-  }
   Site nA = new_site<R>(l, 4, k), nB = new_site<R>(k, 4, r);
   emit<R>(j, k, P<R>(nA), false, P<R>(nB), true);
   bool ok = check_site<R>("resplit.left", b, nA, 4, 4 * l, 4 * r);
@@ -861,10 +905,10 @@ static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, in
     d2h(E.h_info, E.d_info->p, sizeof(int64_t) * 6);
     sync();
     *baseline = E.h_info[0];
-    if (E.h_info[1]) E.counters[4]++;
+    nonconverged(E.h_info[1]);
     if (ns) {
       extents[0] = E.h_info[3];
-      if (E.h_info[4]) E.counters[4]++;
+      nonconverged(E.h_info[4]);
     }
     const bool take = ns && E.h_info[5] != 0;
     const int64_t k = take ? extents[0] : *baseline;
@@ -1046,6 +1090,7 @@ static void batch_extents(mb_chain& c, int nb, const int* bonds, const int* mine
   for (size_t k = 0; k < jobs.size(); ++k) {
     const int t = owner[k] / 2;
     (owner[k] % 2 ? ext_out : base_out)[t] = info[3 * k];
+    nonconverged(info[3 * k + 1]);
   }
 }
 
@@ -1141,8 +1186,8 @@ static void truncate_sweep(mb_chain& c, double eps, int64_t chi) {
     int64_t rprev = outs[0].r;
     for (int t = 0; t < pk.n; ++t) {
       const int64_t k = E.h_sw_info[3 * t];
-      if (E.h_sw_info[3 * t + 1]) E.counters[4]++;
       E.counters[2] += E.h_sw_info[3 * t + 2];
+      nonconverged(E.h_sw_info[3 * t + 1]);
       c.s[outs[t].site] = Site{outs[t].a, k, rprev};
       rprev = k;
     }
@@ -1533,17 +1578,31 @@ static void trial_pair(mb_chain& l, int nl, const int* kl, const int* ql, const 
   } catch (const std::exception& e) {
     main_err = e.what();
     main_code = MB_ERR_ARG;
+  } catch (...) {
+    // the worker still references this frame: never unwind before wait()
+    main_err = "unknown error in the main trial";
+    main_code = MB_ERR_ARG;
   }
   worker.wait();
   ck(cudaStreamSynchronize(A.stream), "aux sync");
   for (auto& st : r.s)
     if (st.b && st.b->s == A.stream) st.b->s = M.stream;
   for (int i = 0; i < 8; ++i) {
-    M.counters[i] += A.counters[i];
+    // slot 5 is a maximum (largest p seen), the others are counts
+    if (i == 5) M.counters[i] = std::max(M.counters[i], A.counters[i]);
+    else M.counters[i] += A.counters[i];
     A.counters[i] = 0;
   }
-  M.recs.insert(M.recs.end(), A.recs.begin(), A.recs.end());
-  A.recs.clear();
+  if (A.prof) {
+    ProfScope::harvest(A, true);
+    for (int i = 0; i < 6; ++i) {
+      M.pms[i] += A.pms[i];
+      M.pfl[i] += A.pfl[i];
+      M.pn[i] += A.pn[i];
+      A.pms[i] = A.pfl[i] = 0;
+      A.pn[i] = 0;
+    }
+  }
   if (main_code) throw MbError(main_code, main_err);
   if (aux_code) throw MbError(aux_code, aux_err);
 }
@@ -1620,12 +1679,13 @@ long long mb_launch_count(void) { return launch_count(); }
 int mb_profile_begin(void) {
   MB_TRY({
     ensure_ready();
-    for (auto& r : E.recs) {
-      E.pool.push_back(r.a);
-      E.pool.push_back(r.b);
+    ProfScope::harvest(E, true);
+    for (int i = 0; i < 6; ++i) {
+      E.pms[i] = E.pfl[i] = 0;
+      E.pn[i] = 0;
     }
-    E.recs.clear();
     E.prof = true;
+    eig_profile_set(true);
     return 0;
   });
 }
@@ -1634,22 +1694,21 @@ int mb_profile_end(double* ms, long long* launches, double* flops) {
   MB_TRY({
     ensure_ready();
     ck(cudaStreamSynchronize(E.stream), "profile sync");
+    ProfScope::harvest(E, true);
     for (int i = 0; i < 6; ++i) {
-      ms[i] = 0;
-      launches[i] = 0;
-      flops[i] = 0;
+      ms[i] = E.pms[i];
+      launches[i] = E.pn[i];
+      flops[i] = E.pfl[i];
     }
-    for (auto& r : E.recs) {
-      float t = 0;
-      cudaEventElapsedTime(&t, r.a, r.b);
-      ms[r.cls] += t;
-      launches[r.cls] += 1;
-      flops[r.cls] += r.flops;
-      E.pool.push_back(r.a);
-      E.pool.push_back(r.b);
-    }
-    E.recs.clear();
     E.prof = false;
+    eig_profile_set(false);
+    return 0;
+  });
+}
+
+int mb_profile_eig(double* ms, long long* launches, double* bytes, double* flops) {
+  MB_TRY({
+    eig_profile_read(ms, launches, bytes, flops);
     return 0;
   });
 }
@@ -1920,6 +1979,42 @@ int mb_svd_truncate(const double* a, int64_t m, int64_t n, int dtype, double eps
     require(eps >= 0 && chi >= 1, "bad truncation parameters");
     if (dtype == MB_C64) svd_host<float>(a, m, n, eps, chi, u, s, v, rank, disc);
     else svd_host<double>(a, m, n, eps, chi, u, s, v, rank, disc);
+    return 0;
+  });
+}
+
+int mb_debug_fail_svd(int n) {
+  force_svd_failures(n);
+  return 0;
+}
+
+int mb_herm_eig(const double* a, int64_t n, double* w, double* v) {
+  MB_TRY({
+    ensure_ready();
+    require(n >= 1, "empty matrix");
+    // host row-major Hermitian -> device column-major (= the transpose)
+    std::vector<double> col((size_t)(2 * n * n));
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t c = 0; c < n; ++c) {
+        col[2 * (r + c * n)] = a[2 * (r * n + c)];
+        col[2 * (r + c * n) + 1] = a[2 * (r * n + c) + 1];
+      }
+    Buf dG = alloc((size_t)(n * n) * sizeof(cx<double>));
+    Buf dV = alloc((size_t)(n * n) * sizeof(cx<double>));
+    Buf dw = alloc((size_t)n * sizeof(double));
+    h2d(dG->p, col.data(), col.size() * sizeof(double));
+    void* ws = grow(E.eigws, eig_workspace_bytes(n));
+    const int fail = herm_eig_device((const cx<double>*)dG->p, n, (double*)dw->p,
+                                     (cx<double>*)dV->p, ws, E.stream);
+    d2h(col.data(), dV->p, col.size() * sizeof(double));
+    d2h(w, dw->p, (size_t)n * sizeof(double));
+    sync();
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t c = 0; c < n; ++c) {
+        v[2 * (r * n + c)] = col[2 * (r + c * n)];
+        v[2 * (r * n + c) + 1] = col[2 * (r + c * n) + 1];
+      }
+    if (fail) throw MbError(MB_ERR_NUMERIC, "tridiagonal QL did not converge");
     return 0;
   });
 }

@@ -2020,6 +2020,60 @@ static int count_bad(const cx<R>* x, int64_t n, cudaStream_t s) {
   return *h;
 }
 
+// Test hook (mb_debug_fail_svd): the next n large-path convergence outcomes
+// are reported as failures, to exercise the perturbed retry and the error.
+static std::atomic<int> g_force_fail{0};
+void force_svd_failures(int n) { g_force_fail.store(n); }
+static bool consume_forced_failure() {
+  int v = g_force_fail.load();
+  while (v > 0 && !g_force_fail.compare_exchange_weak(v, v - 1)) {
+  }
+  return v > 0;
+}
+
+// X += 1e-14 sqrt(fro2) * h(e), h a fixed hash of the element index in [-1, 1)
+template <typename R>
+__global__ void k_perturb(cx<R>* __restrict__ X, int64_t n, const double* __restrict__ fro2) {
+  const double sc = 1e-14 * sqrt(*fro2);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = (uint64_t)e * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 29;
+    const double a = (double)(h >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+    h *= 0x94D049BB133111EBull;
+    h ^= h >> 32;
+    const double b = (double)(h >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+    X[e].x += (R)(sc * a);
+    X[e].y += (R)(sc * b);
+  }
+}
+
+// Sorted spectrum (descending) and the truncation rule of a finished large
+// job whose sig[p, 2p) holds the singular values (Jacobi or Gram path).
+template <typename R>
+void finish_large(SvdJob<R>& J, int conv, int sweeps, cudaStream_t s) {
+  const int64_t p = J.m < J.n ? J.m : J.n;
+  if (p <= 2048) {
+    static const bool attr = (cudaFuncSetAttribute(k_sort_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024),
+                              true);
+    (void)attr;
+    k_sort_rank<R><<<1, 1024, 2 * p * sizeof(R), s>>>(J, p, conv, sweeps + 1);
+    MB_LAUNCH_CHECK();
+  } else {
+    k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
+    MB_LAUNCH_CHECK();
+    const size_t sm = (size_t)p * sizeof(R);
+    static const bool attr =
+        (cudaFuncSetAttribute(k_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true);
+    (void)attr;
+    k_rank<R><<<1, 256, sm, s>>>(J, p, conv, sweeps + 1);
+    MB_LAUNCH_CHECK();
+  }
+}
+
 template <typename R>
 void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
   static const int dbg = env_int("MB_CHECK_SITES", 0);
@@ -2045,6 +2099,17 @@ void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
   if (!precond) {
     // the final check launch leaves the column norms in sig[p, 2p)
     jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps, J.A != nullptr, J.sig + p);
+    if (consume_forced_failure()) conv = 0;
+    if (!conv) {
+      // one retry on a deterministically perturbed copy (tensor.py:139-150):
+      // X V^H + delta with |delta| ~ 1e-14 |A|_F, then sweep on
+      k_perturb<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, ws.red_dev + kSumBlocks);
+      MB_LAUNCH_CHECK();
+      int sweeps2 = 0;
+      jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps2, false, J.sig + p);
+      if (consume_forced_failure()) conv = 0;
+      sweeps += sweeps2;
+    }
     plog.mark(sweeps ? "sweeps" : "check");
   } else {
     // 1. X0 = Q R (Householder, in the workspace copy)
@@ -2116,23 +2181,7 @@ void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
       }
     }
   }
-  if (p <= 2048) {
-    static const bool attr = (cudaFuncSetAttribute(k_sort_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   227 * 1024),
-                              true);
-    (void)attr;
-    k_sort_rank<R><<<1, 1024, 2 * p * sizeof(R), s>>>(J, p, conv, sweeps + 1);
-    MB_LAUNCH_CHECK();
-  } else {
-    k_sort_desc<R><<<(int)cdiv(p, 256), 256, 0, s>>>(J.sig + p, p, J.sig, J.perm);
-    MB_LAUNCH_CHECK();
-    const size_t sm = (size_t)p * sizeof(R);
-    static const bool attr =
-        (cudaFuncSetAttribute(k_rank<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true);
-    (void)attr;
-    k_rank<R><<<1, 256, sm, s>>>(J, p, conv, sweeps + 1);
-    MB_LAUNCH_CHECK();
-  }
+  finish_large<R>(J, conv, sweeps, s);
   plog.mark("sort+rank");
 }
 
@@ -2537,6 +2586,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
                                 cudaStream_t);                                                  \
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
   template void svd_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                     \
+  template void finish_large<R>(SvdJob<R>&, int, int, cudaStream_t);                            \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
   template void qr_explicit<R>(cx<R>*, cx<R>*, cx<R>*, int64_t, int64_t, cudaStream_t);        \
   template void launch_qr_emit<R>(const cx<R>*, const cx<R>*, int64_t, int64_t, bool, cx<R>*,   \

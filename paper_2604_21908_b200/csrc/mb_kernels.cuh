@@ -153,6 +153,14 @@ void svd_large(SvdJob<R>& job, const LargeScratch& ws, cudaStream_t s);
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n);
 
+// Test hook: report the next n large-path convergence outcomes as failures.
+void force_svd_failures(int n);
+
+// Sort sig[p, 2p) descending into sig[0, p) / perm and apply the truncation
+// rule (tensor.py:119-136) for a finished large job.
+template <typename R>
+void finish_large(SvdJob<R>& J, int conv, int sweeps, cudaStream_t s);
+
 // Householder QR (zgeqrf conventions) of the column-major X (q x p) in place,
 // explicit Q into Y; tau needs p entries.
 template <typename R>

@@ -13,6 +13,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native as nat
+from ._native import SvdConvergenceError  # noqa: F401  (reference name, tensor.py:26)
 
 TIE_TOLERANCE = 1e-12
 
@@ -101,3 +102,20 @@ def device_gemm(a: np.ndarray, b: np.ndarray, dtype: str = "complex64",
     nat.check(lib.mb_gemm(nat.dptr(a), nat.dptr(b), m, n, k, nat.DTYPES[dtype],
                           int(bool(tensor_cores)), nat.dptr(c)), "mb_gemm")
     return c
+
+
+def device_herm_eig(a: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Eigen-decomposition of a Hermitian matrix by the engine's large-SVD
+    eigensolver (Householder tridiagonalization, divide and conquer,
+    back-transformation; mb_eig.cu): (w ascending, V with eigenvector
+    columns). The Gram eigenproblem behind svd_truncate's large path."""
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    n, n2 = a.shape
+    if n != n2:
+        raise ValueError("matrix must be square")
+    w = np.empty(n, dtype=np.float64)
+    v = np.empty((n, n), dtype=np.complex128)
+    lib = nat.load()
+    nat.check(lib.mb_herm_eig(nat.dptr(a), n, w.ctypes.data_as(C.POINTER(C.c_double)),
+                              nat.dptr(v)), "mb_herm_eig")
+    return w, v

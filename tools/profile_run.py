@@ -28,6 +28,10 @@ def main():
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--side", default="adaptive")
     ap.add_argument("--chi", type=int, default=8192)
+    ap.add_argument("--deadline", type=float, default=None, help="stop after this many seconds")
+    ap.add_argument("--chunk", type=int, default=8)
+    ap.add_argument("--serial", action="store_true", help="sequential adaptive trials")
+    ap.add_argument("--trace-out", default=None, help="write the trace records (JSON lines)")
     a = ap.parse_args()
     inst = _instance(a.config)
     nat.load()
@@ -36,11 +40,12 @@ def main():
     if a.profile:
         nat.profile_begin()
     t0 = time.perf_counter()
-    job = Contraction(inst.circuit, ContractionConfig(dtype=a.dtype, side_mode=a.side, chi_max=a.chi))
+    job = Contraction(inst.circuit, ContractionConfig(dtype=a.dtype, side_mode=a.side, chi_max=a.chi,
+                                                          concurrent_trials=not a.serial))
     last = t0
     done = False
     while not done:
-        done = job.advance(max_steps=8 if a.max_steps is None else min(8, a.max_steps))
+        done = job.advance(max_steps=a.chunk if a.max_steps is None else min(a.chunk, a.max_steps))
         now = time.perf_counter()
         tr = job.trace[-1] if job.trace else None
         print(f"t={now - t0:8.2f}s steps={job.step} consumed={job.consumed} "
@@ -48,6 +53,8 @@ def main():
               f"unswaps={job.unswap_calls} dt={now - last:.2f}s", flush=True)
         last = now
         if a.max_steps is not None and job.step >= a.max_steps:
+            break
+        if a.deadline is not None and now - t0 > a.deadline:
             break
     out = {}
     if done:
@@ -58,6 +65,7 @@ def main():
     wall = time.perf_counter() - t0
     if a.profile:
         out["profile"] = nat.profile_end()
+        out["profile_eig"] = nat.profile_eig()
     c1 = nat.counters()
     out["wall_s"] = wall
     out["launches"] = nat.launch_count() - l0
@@ -66,6 +74,10 @@ def main():
     out["consumed"] = job.consumed
     out["unswap_calls"] = job.unswap_calls
     out["max_elements"] = max(t.elements for t in job.trace) if job.trace else 0
+    if a.trace_out:
+        with open(a.trace_out, "w") as f:
+            for t in job.trace:
+                f.write(json.dumps([t.phase, t.unitaries_consumed, t.elements, round(t.wall_time_s, 3)]) + "\n")
     print(json.dumps(out, indent=1, default=str))
 
 
