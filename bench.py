@@ -2,16 +2,18 @@
 """Benchmark: middle-MPO contraction of a peaked circuit to its peak
 bitstring on B200 (BASELINE.json metric).
 
-Default workload: configs[1], the 20-qubit peaked circuit with swap
-insertion (the largest configuration whose full contraction both the B200
-arm and the CPU reference arm complete; its trace is golden-verified against
-the reference). ``--config c56`` runs the 56-qubit H2-scale instance
-(configs[3]) — see DESIGN.md for its status.
+Default workload: configs[3], the 56-qubit H2-scale obfuscated peaked circuit
+(reference generator, seed 1, 2036 source two-qubit gates, 15838 after linear
+routing) at the paper's settings (eps 2e-3, chi_max 8192, tau 1e6, adaptive
+side choice). ``--config c36|c20|c12`` run the other configs.
 
 One step = contract the whole circuit (route, split, absorb/unswap/rewire
 loop, apply to |0..0>) and extract the peak on the device. ``value`` is
 source two-qubit gates absorbed per second over the K timed steps (the
 metric's "gates absorbed/s"); ``ms_per_step`` is the wall-clock to peak.
+Warm-up steps on c36/c56 are bounded prefixes of the same contraction (the
+first 64 absorption steps: every kernel family loaded, pools and pinned
+buffers sized); the timed steps are full contractions.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--config c56|c36|c20|c12] [--dtype complex128|complex64]
@@ -19,9 +21,10 @@ metric's "gates absorbed/s"); ``ms_per_step`` is the wall-clock to peak.
 Under torchrun (N>1) every rank holds a replica of the chain and the
 unswap candidate scoring of each parity batch is sharded over the ranks,
 merged by one NCCL all-reduce (sharding.py): one contraction per step,
-scaling "strong", value = its gates / max-over-ranks time. ``--impl reference`` times the CPU
-reference arm (the oracle restatement of the reference algorithm, bit-exact
-with it) on a bounded prefix of the same contraction, on rank 0 only.
+scaling "strong", value = its gates / max-over-ranks time. ``--impl
+reference`` times the CPU reference arm (the oracle restatement of the
+reference algorithm, bit-exact with it) on a bounded prefix of the same
+contraction, on rank 0 only.
 """
 
 from __future__ import annotations
@@ -55,7 +58,9 @@ def _args():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c20")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c56")
+    ap.add_argument("--warm-prefix", type=int, default=64,
+                    help="absorption steps per warm-up step on c36/c56 (0 = full contractions)")
     ap.add_argument("--dtype", choices=["complex128", "complex64"], default="complex128")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0,
                     help="CPU work per reference-arm sample (seconds, approx.)")
@@ -231,18 +236,91 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-_CLASS_KERNEL = {"svd_small": "k_sweep", "svd_large": "k_jacobi_pair_cl", "gemm": "k_gemm"}
+# the kernel behind each large-SVD stage (mb_eig.cu) and its bound
+_STAGE_KERNEL = {
+    "trd_symv": ("k_trd_symv2", "hbm"),
+    "trd_panel": ("k_trd_upd/k_trd_vec", "latency"),
+    "trd_update": ("k_gemm_cm<zd,zd,N,C>", "fp64"),
+    "gram": ("k_gemm_cm<cx,zd,C,N>", "fp64"),
+    "backtransform": ("k_gemm_cm<zd,zd,*,*>", "fp64"),
+    "xv": ("k_gemm_cm<cx,cx,N,N>", "fp64"),
+    "dc": ("k_dc_*", "latency"),
+}
 
 
-def _traffic(cls):
-    """DRAM bytes per launch of the class's dominant kernel, from the committed
-    ncu --set full capture (profiles/r01_kernel_traffic.json), else None."""
-    p = ROOT / "profiles" / "r01_kernel_traffic.json"
+def _fp64_peak(torch):
+    """Measured fp64 GEMM throughput of this GPU (cuBLAS DGEMM 8192^3, best of
+    5, CUDA events): the denominator for the fp64 CUDA-core stages
+    (MEASURED_PEAKS.json holds no fp64 figure). Untimed, before warm-up."""
     try:
-        k = json.loads(p.read_text())["kernels"].get(_CLASS_KERNEL.get(cls, ""))
-    except (OSError, ValueError, KeyError):
+        a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+        b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+        a @ b
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del a, b
+        torch.cuda.empty_cache()
+        return 2.0 * 8192 ** 3 / (best / 1e3) / 1e12
+    except Exception:  # pragma: no cover
         return None
-    return None if k is None else {"kernel": _CLASS_KERNEL[cls], "dram_bytes_per_launch": k["mean"]}
+
+
+def _stage_traffic():
+    """DRAM bytes per launch / algorithmic bytes per launch of the top kernels,
+    from the committed ncu --set full capture (profiles/r02_kernel_traffic.json)."""
+    p = ROOT / "profiles" / "r02_kernel_traffic.json"
+    try:
+        return json.loads(p.read_text())
+    except (OSError, ValueError):
+        return None
+
+
+def _roofline(prof, stages, hbm, src, fp64, dev_ms):
+    """Roofline of the dominant kernel of the timed region: the large-SVD
+    stage with the most device time (its algorithmic bytes / flops per launch
+    over its CUDA-event-measured launch time), HBM-bound stages against the
+    measured copy bandwidth, fp64 GEMM stages against the measured DGEMM."""
+    tot = sum(v["ms"] for v in prof.values()) or 1.0
+    name, st = max(stages.items(), key=lambda kv: kv[1]["ms"])
+    if st["ms"] <= 0:  # small configs never reach the large-SVD path
+        cls, d = max(prof.items(), key=lambda kv: kv[1]["ms"])
+        return {"kernel_class": cls, "bound": "latency", "achieved": None, "peak": None,
+                "unit": None, "frac": None, "traffic": None,
+                "share_of_profiled_device_time": d["ms"] / tot,
+                "note": "no large-SVD stage ran; small dependent factorizations (latency-bound)"}
+    kernel, bound = _STAGE_KERNEL[name]
+    traffic = _stage_traffic()
+    out = {"kernel": kernel, "stage": name, "launches": st["launches"],
+           "ms_total": round(st["ms"], 3),
+           "ms_per_launch": st["ms"] / max(st["launches"], 1),
+           "share_of_profiled_device_time": st["ms"] / tot,
+           "share_of_step": st["ms"] / dev_ms if dev_ms else None,
+           "algorithmic_bytes_per_launch": st["bytes"] / max(st["launches"], 1),
+           "algorithmic_flops_per_launch": st["flops"] / max(st["launches"], 1),
+           "traffic": (traffic or {}).get(kernel.split("/")[0], {}).get("dram_bytes_per_launch")
+           if traffic else None,
+           "traffic_source": "profiles/r02_kernel_traffic.json (ncu --set full)" if traffic else None}
+    if bound == "hbm" or bound == "latency":
+        ach = st["bytes"] / (st["ms"] / 1e3) / 1e9 if st["ms"] else 0.0
+        out.update({"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"})
+    else:
+        ach = st["flops"] / (st["ms"] / 1e3) / 1e12 if st["ms"] else 0.0
+        out.update({"bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+                    "frac": ach / fp64 if fp64 else None,
+                    "peak_source": "cuBLAS DGEMM 8192^3 measured in bench.py (no fp64 figure in MEASURED_PEAKS.json)"})
+    out["stages"] = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
+                         "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else None,
+                         "TFLOP/s": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 2) if v["ms"] else None}
+                     for k, v in stages.items()}
+    return out
 
 
 def _phase_seconds(trace):
@@ -297,6 +375,7 @@ def main():
     cfg = ContractionConfig(dtype=args.dtype,
                             unswap_strategy="parity-batched" if world > 1 else "parity-parallel")
     n2q = inst.circuit.two_qubit_count()
+    big = args.config in ("c36", "c56")
 
     def one_step():
         job = Contraction(inst.circuit, cfg, comm)
@@ -304,22 +383,33 @@ def main():
         res = job.finish()
         return job, peak_output(res)
 
+    def warm_step():
+        if big and args.warm_prefix > 0:
+            Contraction(inst.circuit, cfg, comm).advance(max_steps=args.warm_prefix)
+        else:
+            one_step()
+
     def barrier():
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         nat.synchronize()
 
+    fp64 = _fp64_peak(torch) if rank == 0 else None
     for _ in range(args.warmup):
-        one_step()
+        warm_step()
     barrier()
 
     # ---- timed region: device-resident path (circuit already loaded) ----
+    # per-class and per-stage CUDA events run inside it (the roofline's kernel
+    # durations are measured live, on the engine streams)
     clocks = Clocks()
     clocks.start()
     launches0 = nat.launch_count()
+    c_t0 = nat.counters()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    nat.profile_begin()
     ev0.record(stream)
     peaks, jobs = [], []
     for _ in range(args.steps):
@@ -328,7 +418,10 @@ def main():
         jobs.append(job)
     ev1.record(stream)
     barrier()
+    prof = nat.profile_end()
+    stages = nat.profile_eig()
     clk = clocks.stop()
+    c_t1 = nat.counters()
     dev_ms = ev0.elapsed_time(ev1)
     launches = nat.launch_count() - launches0
     t_dev = "cuda" if not dist or dist.get_backend() == "nccl" else "cpu"
@@ -361,17 +454,11 @@ def main():
     h2d = (c1["h2d_bytes"] - c0["h2d_bytes"]) // args.steps + len(qasm)
     d2h = (c1["d2h_bytes"] - c0["d2h_bytes"]) // args.steps
 
-    # ---- one profiled (untimed) step: per-kernel-class device time ----
-    nat.profile_begin()
-    one_step()
-    prof = nat.profile_end()
-    hbm, bf16, src = _peaks()
-    dom = max(prof, key=lambda k: prof[k]["ms"])
-    tot_ms = sum(v["ms"] for v in prof.values())
-    d = prof[dom]
-    achieved_tf = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
-
     if rank == 0:
+        hbm, bf16, src = _peaks()
+        roof = _roofline(prof, stages, hbm, src, fp64, dev_ms)
+        counters = {k: c_t1[k] - c_t0[k] for k in c_t1 if k != "max_p"}
+        counters["max_p"] = c_t1["max_p"]
         line = {
             "metric": METRIC, "value": value, "unit": "source 2q gates absorbed/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -382,26 +469,30 @@ def main():
             "config": dict(_workload(args.config, args.dtype),
                            parallelism=(f"sharded unswap scoring x{world} (NCCL all-reduce)"
                                         if world > 1 else "1 GPU"),
-                           unswap_order="parity-batched" if world > 1 else "parity-parallel"),
+                           unswap_order="parity-batched" if world > 1 else "parity-parallel",
+                           warmup_steps=(f"first {args.warm_prefix} absorption steps" if big and args.warm_prefix
+                                         else "full contractions"),
+                           timed_region="per-class / per-stage CUDA events on (roofline durations)"),
             "peak": {"bits": peaks[-1][0], "probability": peaks[-1][1],
-                     "planted": inst.peak, "match": peaks[-1][0] == inst.peak},
+                     "planted": inst.peak, "match": peaks[-1][0] == inst.peak,
+                     "e2e_bits_match": bits == peaks[-1][0]},
             "two_qubit_gates": n2q,
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": {"value": total_gates / (e2e_ms / 1e3), "unit": "source 2q gates absorbed/s",
                     "ms_per_step": e2e_ms / args.steps,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-            "roofline": {"bound": "tensor", "kernel_class": dom, "achieved": achieved_tf,
-                         "peak": bf16, "unit": "TFLOP/s", "frac": achieved_tf / bf16,
-                         "traffic": _traffic(dom), "peak_source": src,
-                         "share_of_device_time": d["ms"] / tot_ms if tot_ms else None,
-                         "note": "fp64/fp32 CUDA-core Jacobi + GEMM vs the bf16 tensor peak"},
+            "roofline": roof,
             "profile_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "svd_large_stages_ms": {k: round(v["ms"], 3) for k, v in stages.items()},
             "contraction": {"trace_records": len(jobs[-1].trace), "unswap_calls": jobs[-1].unswap_calls,
                             "phase_s": _phase_seconds(jobs[-1].trace),
                             "accepted_swaps": jobs[-1].accepted_swaps,
+                            "absorb_steps": jobs[-1].step,
+                            "unitaries_consumed": jobs[-1].consumed,
+                            "chi_saturations": jobs[-1].chi_saturations,
                             "max_elements": max(t.elements for t in jobs[-1].trace)},
-            "counters": nat.counters(),
+            "counters": counters,
         }
         if not args.no_cpu_baseline and world == 1:
             steps = cpu_prefix_steps(args.config, args.cpu_sample_s)

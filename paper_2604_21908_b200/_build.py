@@ -33,6 +33,11 @@ def up_to_date() -> bool:
     return all(d.stat().st_mtime <= t for d in deps)
 
 
+def _flags() -> list:
+    # MB_DEBUG_BUILD=1 compiles in the debug-only logs / dumps (mb_debug_env)
+    return FLAGS + (["-DMB_DEBUG_LOGS=1"] if os.environ.get("MB_DEBUG_BUILD") == "1" else [])
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return OUT
@@ -40,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs, procs = [], []
     for src in SOURCES:  # the translation units are independent: compile them concurrently
         obj = OUT.parent / (Path(src).stem + ".o")
-        cmd = [_nvcc(), *ARCH, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [_nvcc(), *ARCH, *_flags(), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd))
         procs.append((cmd, subprocess.Popen(cmd)))

@@ -8,9 +8,26 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <cmath>
 
 namespace mb {
+
+// Debug-only environment switches (shape/timing logs, matrix dumps, site
+// checks) exist only in builds with -DMB_DEBUG_LOGS=1 (MB_DEBUG_BUILD=1 in
+// _build.py); in release builds this returns nullptr at compile time and the
+// synchronizing debug paths are dead code.
+#ifndef MB_DEBUG_LOGS
+#define MB_DEBUG_LOGS 0
+#endif
+inline const char* mb_debug_env(const char* name) {
+#if MB_DEBUG_LOGS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 template <typename R>
 struct alignas(2 * sizeof(R)) cx {

@@ -214,10 +214,18 @@ constexpr int TBM = 64, TBN = 64;
 
 template <typename TI, typename TC, bool CA, bool CB, int BK>
 __global__ void __launch_bounds__(256) k_gemm_cm(const GemmDesc* __restrict__ descs, GemmDesc one,
-                                                 double alpha, double beta) {
+                                                 double alpha, double beta, int64_t kslice) {
   __shared__ TC As[BK][TBM + 1];
   __shared__ TC Bs[BK][TBN + 1];
-  const GemmDesc d = descs ? descs[blockIdx.z] : one;
+  GemmDesc d = descs ? descs[blockIdx.z] : one;
+  int64_t kbeg = 0;
+  if (!descs && kslice > 0) {
+    // split-K: slice z covers K range [z kslice, (z+1) kslice) and writes its
+    // partial product to C + z ldc N (summed by k_splitk_reduce)
+    kbeg = (int64_t)blockIdx.z * kslice;
+    d.K = min(d.K, kbeg + kslice);
+    d.C = (void*)((TC*)d.C + (int64_t)blockIdx.z * d.ldc * d.N);
+  }
   const int64_t M = d.M, N = d.N, K = d.K;
   const int64_t m0 = (int64_t)blockIdx.x * TBM, n0 = (int64_t)blockIdx.y * TBN;
   if (m0 >= M || n0 >= N) return;
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(256) k_gemm_cm(const GemmDesc* __restrict__ de
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = Tr<TC>::zero();
-  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+  for (int64_t k0 = kbeg; k0 < K; k0 += BK) {
 #pragma unroll
     for (int t = 0; t < (TBM * BK) / 256; ++t) {
       const int e = tid + 256 * t;
@@ -299,7 +307,54 @@ static void gemm_cm(int stage, int64_t M, int64_t N, int64_t K, double alpha, co
   GemmDesc d{M, N, K, A, lda, B, ldb, C, ldc};
   constexpr int BK = sizeof(TC) >= 16 ? 8 : 16;
   dim3 grid((unsigned)ediv(M, TBM), (unsigned)ediv(N, TBN), 1);
-  k_gemm_cm<TI, TC, CA, CB, BK><<<grid, 256, 0, s>>>(nullptr, d, alpha, beta);
+  k_gemm_cm<TI, TC, CA, CB, BK><<<grid, 256, 0, s>>>(nullptr, d, alpha, beta, 0);
+  EIG_CHECK();
+}
+
+template <typename TC>
+__global__ void k_splitk_reduce(const TC* __restrict__ P, int nsl, int64_t M, int64_t N,
+                                TC* __restrict__ C, int64_t ldc, double alpha, double beta) {
+  const int64_t tot = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % M, c = e / M;
+    TC acc = P[e];
+    for (int z = 1; z < nsl; ++z) acc = Tr<TC>::add(acc, P[e + (int64_t)z * tot]);
+    TC v = Tr<TC>::scale(acc, alpha);
+    if (beta != 0.0) v = Tr<TC>::add(v, Tr<TC>::scale(C[r + c * ldc], beta));
+    C[r + c * ldc] = v;
+  }
+}
+
+// C = alpha op(A) op(B) + beta C with K split over slices when the output
+// grid alone cannot fill the chip (skinny M x N, long K); partials in `part`
+// (nsl * M * N elements), fixed-order reduction.
+template <typename TI, typename TC, bool CA, bool CB>
+static void gemm_cm_splitk(int stage, int64_t M, int64_t N, int64_t K, double alpha, const TI* A,
+                           int64_t lda, const TI* B, int64_t ldb, double beta, TC* C, int64_t ldc,
+                           TC* part, int64_t part_cap, cudaStream_t s) {
+  const int64_t tiles = ediv(M, TBM) * ediv(N, TBN);
+  int nsl = (int)std::min<int64_t>(std::max<int64_t>(1, (2 * 148) / std::max<int64_t>(1, tiles)),
+                                   std::max<int64_t>(1, K / 256));
+  nsl = (int)std::min<int64_t>(nsl, part_cap / std::max<int64_t>(1, M * N));
+  if (nsl <= 1) {
+    gemm_cm<TI, TC, CA, CB>(stage, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s);
+    return;
+  }
+  const double by = (double)sizeof(TI) * (double)(M * K + K * N) +
+                    (double)sizeof(TC) * (double)(M * N) * (beta != 0.0 ? 2.0 : 1.0);
+  const double fl = (sizeof(TC) == sizeof(double) ? 2.0 : 8.0) * (double)M * (double)N * (double)K;
+  EigScope sc(stage, s, by, fl);
+  constexpr int BK = sizeof(TC) >= 16 ? 8 : 16;
+  int64_t ks = ediv(K, nsl);
+  ks = ediv(ks, BK) * BK;
+  nsl = (int)ediv(K, ks);
+  GemmDesc d{M, N, K, A, lda, B, ldb, part, M};
+  dim3 grid((unsigned)ediv(M, TBM), (unsigned)ediv(N, TBN), (unsigned)nsl);
+  k_gemm_cm<TI, TC, CA, CB, BK><<<grid, 256, 0, s>>>(nullptr, d, 1.0, 0.0, ks);
+  EIG_CHECK();
+  k_splitk_reduce<TC><<<(int)std::min<int64_t>(ediv(M * N, 256), 148 * 8), 256, 0, s>>>(
+      part, nsl, M, N, C, ldc, alpha, beta);
   EIG_CHECK();
 }
 
@@ -334,7 +389,7 @@ __global__ void k_count_nonfinite(const double* __restrict__ x, int64_t n, int* 
 }
 
 static bool eig_debug() {
-  static const bool on = getenv("MB_EIG_DEBUG") && atoi(getenv("MB_EIG_DEBUG"));
+  static const bool on = mb_debug_env("MB_EIG_DEBUG") && atoi(mb_debug_env("MB_EIG_DEBUG"));
   return on;
 }
 
@@ -358,6 +413,67 @@ static void dbg_check(const char* what, const void* p, int64_t ndoubles, cudaStr
 // indexed by global row. pv: p1 = V^H v in [0, kNB), p2 = W^H v in [kNB, 2 kNB).
 
 constexpr int kNB = 32;
+constexpr int kNBT = 64;       // reflectors per back-transformation block
+constexpr int kMaxSplit = 8;   // split-K slices
+
+// a -= sum_{t<i} V[r,t] conj(rw[t]) + W[r,t] conj(rv[t]); W[r, t_over] is
+// replaced by w_over. Loads are issued eight at a time (independent), so a
+// row costs a few memory latencies instead of 2 i dependent ones.
+__device__ __forceinline__ zd panel_row_update(zd a, const zd* __restrict__ V,
+                                               const zd* __restrict__ W, int64_t r, int64_t n,
+                                               int i, const zd* rv, const zd* rw, int t_over,
+                                               zd w_over) {
+  for (int t0 = 0; t0 < i; t0 += 8) {
+    zd vv[8], ww[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u;
+      if (t < i) {
+        vv[u] = V[r + t * n];
+        ww[u] = (t == t_over) ? w_over : W[r + t * n];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u;
+      if (t < i) {
+        a = csub(a, cmul(vv[u], cconj(rw[t])));
+        a = csub(a, cmul(ww[u], cconj(rv[t])));
+      }
+    }
+  }
+  return a;
+}
+
+// sum over k in [k0, n) of conj(col[k]) v[k], lanes strided, four loads in
+// flight per lane
+__device__ __forceinline__ zd col_dot(const zd* __restrict__ col, const zd* __restrict__ v,
+                                      int64_t k0, int64_t n, int lane) {
+  double sr = 0, si = 0;
+  int64_t k = k0 + lane;
+  for (; k + 96 < n; k += 128) {
+    const zd a0 = col[k], a1 = col[k + 32], a2 = col[k + 64], a3 = col[k + 96];
+    const zd b0 = v[k], b1 = v[k + 32], b2 = v[k + 64], b3 = v[k + 96];
+    zd t = cmulc(a0, b0);
+    sr += t.x;
+    si += t.y;
+    t = cmulc(a1, b1);
+    sr += t.x;
+    si += t.y;
+    t = cmulc(a2, b2);
+    sr += t.x;
+    si += t.y;
+    t = cmulc(a3, b3);
+    sr += t.x;
+    si += t.y;
+  }
+  for (; k < n; k += 32) {
+    const zd t = cmulc(col[k], v[k]);
+    sr += t.x;
+    si += t.y;
+  }
+  return mk<double>(warp_sum(sr), warp_sum(si));
+}
 
 // Part A (prev >= 0): finish W[:, prev] of column cp = j0 + prev from y:
 //   w = tau y; alpha = -tau/2 (w^H v); w += alpha v.
@@ -408,12 +524,8 @@ __global__ void __launch_bounds__(1024) k_trd_col(zd* __restrict__ A, int64_t n,
   // column update: A[r, c] -= sum_t V[r,t] conj(W[c,t]) + W[r,t] conj(V[c,t])
   double xn = 0;
   for (int64_t r = c + tid; r < n; r += nt) {
-    zd a = A[r + c * n];
-    for (int t = 0; t < i; ++t) {
-      zd vr = V[r + t * n], wr = W[r + t * n];
-      a = csub(a, cmul(vr, cconj(sh_roww[t])));
-      a = csub(a, cmul(wr, cconj(sh_rowv[t])));
-    }
+    const zd a = panel_row_update(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, -1,
+                                  mk<double>(0, 0));
     A[r + c * n] = a;
     if (r >= c + 2) xn += cabs2(a);
   }
@@ -462,6 +574,7 @@ __global__ void __launch_bounds__(1024) k_trd_col(zd* __restrict__ A, int64_t n,
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   for (int t = wid; t < i; t += nw) {
     double p1r = 0, p1i = 0, p2r = 0, p2i = 0;
+#pragma unroll 4
     for (int64_t r = c + 1 + lane; r < n; r += 32) {
       zd v = V[r + i * n];
       zd a = cmulc(V[r + t * n], v);
@@ -494,17 +607,9 @@ __global__ void __launch_bounds__(256) k_trd_symv(const zd* __restrict__ A, int6
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const zd* v = V + (int64_t)i * n;
   for (int64_t r = c + 1 + warp; r < n; r += nwarps) {
-    const zd* col = A + r * n;
-    double sr = 0, si = 0;
-    for (int64_t k = c + 1 + lane; k < n; k += 32) {
-      zd t = cmulc(col[k], v[k]);
-      sr += t.x;
-      si += t.y;
-    }
-    sr = warp_sum(sr);
-    si = warp_sum(si);
+    const zd dot = col_dot(A + r * n, v, c + 1, n, lane);
     if (lane == 0) {
-      zd acc = mk<double>(sr, si);
+      zd acc = dot;
       for (int t = 0; t < i; ++t) {
         acc = csub(acc, cmul(W[r + t * n], pv[t]));
         acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
@@ -514,49 +619,311 @@ __global__ void __launch_bounds__(256) k_trd_symv(const zd* __restrict__ A, int6
   }
 }
 
+
+// Grid-parallel panel step for large trailing blocks (the single-CTA
+// k_trd_col would serialize O(n * 32) complex work per column on one SM).
+// Three launches per column: k_trd_upd (finish W[:, i-1], update column c,
+// partial |x|^2), k_trd_vec (Householder scalars, reflector, partial V^H v and
+// W^H v), k_trd_symv2 (y = A22 v - W p1 - V p2, partial y^H v). All partial
+// sums are reduced in a fixed order (bitwise reproducible).
+constexpr int kRowBlk = 256;    // rows per block in upd / vec
+constexpr int kMaxSymvBlk = 1184;
+constexpr int kPartStride = 4 * kNB + 4;  // doubles per block partial
+
+__device__ __forceinline__ zd fixed_sum_cx(const double* part, int nblk, int off) {
+  // warp-level fixed-order sum of part[b * kPartStride + off .. +1] over b
+  const int lane = threadIdx.x & 31;
+  double re = 0, im = 0;
+  for (int b = lane; b < nblk; b += 32) {
+    re += part[(int64_t)b * kPartStride + off];
+    im += part[(int64_t)b * kPartStride + off + 1];
+  }
+  re = warp_sum(re);
+  im = warp_sum(im);
+  return mk<double>(re, im);
+}
+
+__global__ void __launch_bounds__(kRowBlk) k_trd_upd(zd* __restrict__ A, int64_t n,
+                                                     zd* __restrict__ VW, int64_t j0, int i, int b,
+                                                     double* __restrict__ dd, const zd* __restrict__ tau,
+                                                     const zd* __restrict__ y,
+                                                     const double* __restrict__ part_yv, int nblk_yv,
+                                                     double* __restrict__ part_x) {
+  __shared__ zd sh_rowv[kNB], sh_roww[kNB];
+  __shared__ zd sh_alpha;
+  __shared__ double red[32];
+  zd* V = VW;
+  zd* W = VW + (int64_t)kNB * n;
+  const int64_t c = j0 + i;          // column to update (if i < b)
+  const int64_t r = c + (int64_t)blockIdx.x * kRowBlk + threadIdx.x;
+  const int t_prev = i - 1;
+  zd tp = mk<double>(0, 0);
+  if (i > 0) {
+    tp = tau[c - 1];
+    if (threadIdx.x < 32) {
+      const zd yv = fixed_sum_cx(part_yv, nblk_yv, 0);
+      if (threadIdx.x == 0) {
+        // alpha = -tau/2 (w^H v), w = tau y  =>  w^H v = conj(tau) (y^H v)
+        const zd whv = cmul(cconj(tp), yv);
+        sh_alpha = cmul(mk<double>(-0.5 * tp.x, -0.5 * tp.y), whv);
+      }
+    }
+    __syncthreads();
+  }
+  const zd al = i > 0 ? sh_alpha : mk<double>(0, 0);
+  zd wr = mk<double>(0, 0);
+  if (i > 0 && r < n) {
+    wr = cadd(cmul(tp, y[r]), cmul(al, V[r + t_prev * n]));
+    W[r + t_prev * n] = wr;
+  }
+  if (i >= b) return;
+  // row c of the panel's V and W (t < i); W[c, i-1] recomputed redundantly
+  if (threadIdx.x < i) {
+    const int t = threadIdx.x;
+    sh_rowv[t] = V[c + t * n];
+    sh_roww[t] = (t == t_prev) ? cadd(cmul(tp, y[c]), cmul(al, V[c + t * n])) : W[c + t * n];
+  }
+  __syncthreads();
+  double xn = 0;
+  if (r < n) {
+    const zd a = panel_row_update(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, t_prev, wr);
+    A[r + c * n] = a;
+    if (r == c) dd[c] = a.x;
+    if (r >= c + 2) xn = cabs2(a);
+  }
+  xn = block_sum(xn, red);
+  if (threadIdx.x == 0) part_x[(int64_t)blockIdx.x * kPartStride] = xn;
+}
+
+__global__ void __launch_bounds__(kRowBlk) k_trd_vec(zd* __restrict__ A, int64_t n,
+                                                     zd* __restrict__ VW, int64_t c, int i,
+                                                     double* __restrict__ ee, zd* __restrict__ tau,
+                                                     const double* __restrict__ part_x, int nblk_x,
+                                                     double* __restrict__ part_p) {
+  __shared__ zd sh_sc;
+  __shared__ zd red_w[kRowBlk / 32][2 * kNB];
+  zd* V = VW;
+  zd* W = VW + (int64_t)kNB * n;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double x = 0;
+    for (int bb = lane; bb < nblk_x; bb += 32) x += part_x[(int64_t)bb * kPartStride];
+    x = warp_sum(x);
+    if (lane == 0) {
+      const zd al = A[(c + 1) + c * n];
+      zd tv, sc;
+      double beta;
+      if (x + al.x * al.x + al.y * al.y < 1e-250) {
+        tv = mk<double>(0, 0);
+        beta = al.x;
+        sc = mk<double>(0, 0);
+      } else {
+        beta = -copysign(sqrt(al.x * al.x + al.y * al.y + x), al.x);
+        tv = mk<double>((beta - al.x) / beta, -al.y / beta);
+        const zd den = mk<double>(al.x - beta, al.y);
+        const double dn = den.x * den.x + den.y * den.y;
+        sc = mk<double>(den.x / dn, -den.y / dn);
+      }
+      sh_sc = sc;
+      if (blockIdx.x == 0) {
+        ee[c] = beta;
+        tau[c] = tv;
+      }
+    }
+  }
+  __syncthreads();
+  const zd sc = sh_sc;
+  const int64_t r = c + 1 + (int64_t)blockIdx.x * kRowBlk + threadIdx.x;
+  zd v = mk<double>(0, 0);
+  if (r < n) {
+    if (r == c + 1) {
+      v = mk<double>(1, 0);
+    } else {
+      v = cmul(A[r + c * n], sc);
+      A[r + c * n] = v;
+    }
+    V[r + i * n] = v;
+  }
+  // partial p1 = V[:, t]^H v, p2 = W[:, t]^H v over this block's rows
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t0 = 0; t0 < i; t0 += 8) {
+    zd va[8], wa[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      va[u] = mk<double>(0, 0);
+      wa[u] = mk<double>(0, 0);
+      if (r < n && t0 + u < i) {
+        va[u] = cmulc(V[r + (t0 + u) * n], v);
+        wa[u] = cmulc(W[r + (t0 + u) * n], v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (t0 + u >= i) break;
+      const double ar = warp_sum(va[u].x), ai = warp_sum(va[u].y);
+      const double wr = warp_sum(wa[u].x), wi = warp_sum(wa[u].y);
+      if (lane == 0) {
+        red_w[wid][t0 + u] = mk<double>(ar, ai);
+        red_w[wid][kNB + t0 + u] = mk<double>(wr, wi);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
+    const int t = e < i ? e : kNB + (e - i);
+    zd acc = mk<double>(0, 0);
+    for (int w2 = 0; w2 < kRowBlk / 32; ++w2) acc = cadd(acc, red_w[w2][t]);
+    part_p[(int64_t)blockIdx.x * kPartStride + 2 * t] = acc.x;
+    part_p[(int64_t)blockIdx.x * kPartStride + 2 * t + 1] = acc.y;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_trd_symv2(const zd* __restrict__ A, int64_t n,
+                                                   const zd* __restrict__ VW, int64_t c, int i,
+                                                   const double* __restrict__ part_p, int nblk_p,
+                                                   zd* __restrict__ y, double* __restrict__ part_yv) {
+  __shared__ zd pv[2 * kNB];
+  __shared__ double red_re[8], red_im[8];
+  const zd* V = VW;
+  const zd* W = VW + (int64_t)kNB * n;
+  // p1 / p2 from the vec kernel's partials (fixed order, every block the same)
+  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
+    const int t = e < i ? e : kNB + (e - i);
+    double re = 0, im = 0;
+    for (int bb = 0; bb < nblk_p; ++bb) {
+      re += part_p[(int64_t)bb * kPartStride + 2 * t];
+      im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
+    }
+    pv[t] = mk<double>(re, im);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const zd* v = V + (int64_t)i * n;
+  double yvr = 0, yvi = 0;
+  for (int64_t r = c + 1 + warp; r < n; r += nwarps) {
+    const zd dot = col_dot(A + r * n, v, c + 1, n, lane);
+    if (lane == 0) {
+      zd acc = dot;
+      for (int t = 0; t < i; ++t) {
+        acc = csub(acc, cmul(W[r + t * n], pv[t]));
+        acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
+      }
+      y[r] = acc;
+      const zd yv = cmulc(acc, v[r]);  // conj(y_r) v_r
+      yvr += yv.x;
+      yvi += yv.y;
+    }
+  }
+  if (lane == 0) {
+    red_re[wid] = yvr;
+    red_im[wid] = yvi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, bq = 0;
+    for (int w2 = 0; w2 < 8; ++w2) {
+      a += red_re[w2];
+      bq += red_im[w2];
+    }
+    part_yv[(int64_t)blockIdx.x * kPartStride] = a;
+    part_yv[(int64_t)blockIdx.x * kPartStride + 1] = bq;
+  }
+}
+
+// dst[r, t] = src[r, t] for r < m, t < b (column-major, leading dimension ld)
+__global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, int64_t m, int b,
+                            int64_t ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * b;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % m, t = e / m;
+    dst[r + t * ld] = src[r + t * ld];
+  }
+}
+
 __global__ void k_trd_last(const zd* __restrict__ A, int64_t n, double* __restrict__ dd) {
   dd[n - 1] = A[(n - 1) + (n - 1) * n].x;
 }
 
 static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* pv, zd* y,
-                  cudaStream_t s) {
+                  double* part, cudaStream_t s) {
   if (n == 1) {
     k_trd_last<<<1, 1, 0, s>>>(A, n, d);
     EIG_CHECK();
     return;
   }
+  // partial-sum areas (kMaxSymvBlk blocks each)
+  double* part_x = part;
+  double* part_p = part + (size_t)kMaxSymvBlk * kPartStride;
+  double* part_yv = part + 2 * (size_t)kMaxSymvBlk * kPartStride;
   const int64_t nref = n - 1;
+  int nblk_yv = 0;  // blocks of the previous column's symv (grid path)
   for (int64_t j0 = 0; j0 < nref; j0 += kNB) {
     const int b = (int)std::min<int64_t>(kNB, nref - j0);
+    // one CTA per panel step while the trailing block is small; the grid
+    // path above ~768 rows
+    const bool grid = n - j0 > 768;
     for (int i = 0; i <= b; ++i) {
-      const int threads = n - j0 > 4096 ? 1024 : 512;
-      {
-        const double rows = (double)(n - j0 - i);
+      const int64_t c = j0 + i;
+      const double rows = (double)(n - c);
+      if (!grid) {
+        const int threads = 512;
         EigScope sc(ES_TRD_PANEL, s, 16.0 * rows * (2.0 * i + 4.0), 8.0 * rows * (2.0 * i + 3.0));
         k_trd_col<<<1, threads, 0, s>>>(A, n, VW, j0, i, b, d, e, tau, pv, y);
         EIG_CHECK();
-      }
-      if (i < b) {
-        const int64_t c = j0 + i;
-        const int64_t rows = n - c - 1;
-        if (rows > 0) {
-          const int blocks = (int)std::min<int64_t>(ediv(rows, 8), 148 * 8);
-          // the trailing Hermitian block is read once (rows^2 complex)
-          EigScope sc(ES_TRD_SYMV, s, 16.0 * (double)rows * (double)rows + 16.0 * rows * (2.0 * i + 2.0),
-                      8.0 * (double)rows * (double)rows);
+        if (i < b && n - c - 1 > 0) {
+          const int64_t rw = n - c - 1;
+          const int blocks = (int)std::min<int64_t>(ediv(rw, 8), kMaxSymvBlk);
+          EigScope sc2(ES_TRD_SYMV, s, 16.0 * (double)rw * (double)rw + 16.0 * rw * (2.0 * i + 2.0),
+                       8.0 * (double)rw * (double)rw);
           k_trd_symv<<<blocks, 256, 0, s>>>(A, n, VW, c, i, pv, y);
           EIG_CHECK();
         }
+        continue;
+      }
+      const int nblk_u = (int)ediv(n - c, kRowBlk);
+      {
+        EigScope sc(ES_TRD_PANEL, s, 16.0 * rows * (2.0 * i + 4.0), 8.0 * rows * (2.0 * i + 3.0));
+        k_trd_upd<<<nblk_u, kRowBlk, 0, s>>>(A, n, VW, j0, i, b, d, tau, y, part_yv, nblk_yv, part_x);
+        EIG_CHECK();
+      }
+      if (i >= b) break;
+      const int64_t rw = n - c - 1;
+      const int nblk_v = (int)std::max<int64_t>(1, ediv(rw, kRowBlk));
+      {
+        EigScope sc(ES_TRD_PANEL, s, 16.0 * rows * (2.0 * i + 2.0), 8.0 * rows * (2.0 * i + 1.0));
+        k_trd_vec<<<nblk_v, kRowBlk, 0, s>>>(A, n, VW, c, i, e, tau, part_x, nblk_u, part_p);
+        EIG_CHECK();
+      }
+      {
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ediv(rw, 8), kMaxSymvBlk));
+        EigScope sc(ES_TRD_SYMV, s, 16.0 * (double)rw * (double)rw + 16.0 * rw * (2.0 * i + 2.0),
+                    8.0 * (double)rw * (double)rw);
+        k_trd_symv2<<<blocks, 256, 0, s>>>(A, n, VW, c, i, part_p, nblk_v, y, part_yv);
+        EIG_CHECK();
+        nblk_yv = blocks;
       }
     }
-    // trailing update A22 -= V W^H + W V^H (rows / cols >= j0 + b)
+    // trailing update A22 -= V W^H + W V^H (rows / cols >= j0 + b): for a full
+    // panel one GEMM [V W] [W V]^H (V copied after W), else two
     const int64_t t0 = j0 + b, m = n - t0;
     if (m > 0) {
       const zd* V2 = VW + t0;
       const zd* W2 = VW + (int64_t)kNB * n + t0;
       zd* C = A + t0 + t0 * n;
-      gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, V2, n, W2, n, 1.0, C, n, s);
-      gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, W2, n, V2, n, 1.0, C, n, s);
+      if (b == kNB) {
+        {
+          EigScope sc(ES_TRD_UPDATE, s, 32.0 * (double)(m * b), 0.0);
+          k_copy_cols<<<(int)std::min<int64_t>(ediv(m * b, 256), 148 * 8), 256, 0, s>>>(
+              VW + t0, VW + 2 * (int64_t)kNB * n + t0, m, b, n);
+          EIG_CHECK();
+        }
+        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, 2 * b, -1.0, V2, n, W2, n, 1.0, C, n, s);
+      } else {
+        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, V2, n, W2, n, 1.0, C, n, s);
+        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, W2, n, V2, n, 1.0, C, n, s);
+      }
     }
   }
   k_trd_last<<<1, 1, 0, s>>>(A, n, d);
@@ -870,16 +1237,29 @@ __global__ void __launch_bounds__(128) k_dc_secular(const DcMerge* __restrict__ 
     hi_t = rho * zz;
   }
   const double dorg = d[org];
-  for (int it = 0; it < 300; ++it) {
-    const double t = 0.5 * (lo_t + hi_t);
-    if (t == lo_t || t == hi_t) break;
-    double f = 1.0;
-    for (int j = 0; j < k; ++j) f += rho * z[j] * z[j] / ((d[j] - dorg) - t);
+  // bracketed Newton: f is increasing on the bracket; a Newton step that
+  // leaves the bracket (or stalls) is replaced by bisection
+  double t = 0.5 * (lo_t + hi_t);
+  for (int it = 0; it < 200; ++it) {
+    double f = 1.0, fp = 0.0;
+    for (int j = 0; j < k; ++j) {
+      const double inv = 1.0 / ((d[j] - dorg) - t);
+      const double w = rho * z[j] * z[j] * inv;
+      f += w;
+      fp += w * inv;
+    }
     if (f > 0) hi_t = t;
-    else lo_t = t;
+    else if (f < 0) lo_t = t;
+    else break;
+    const double mid = 0.5 * (lo_t + hi_t);
+    if (mid == lo_t || mid == hi_t) break;
+    double tn = t - f / fp;
+    if (!(tn > lo_t && tn < hi_t)) tn = mid;
+    if (tn == t) break;
+    t = tn;
   }
   S.org[lo + i] = org;
-  S.tau[lo + i] = 0.5 * (lo_t + hi_t);
+  S.tau[lo + i] = t;
 }
 
 // Gu-Eisenstat: zhat_i^2 = (lambda_i - d_i)/rho * prod_{j != i} (lambda_j - d_i)/(d_j - d_i)
@@ -1006,7 +1386,7 @@ struct EigLayout {
 enum {
   L_G, L_VC, L_QA, L_QS, L_SV, L_VW, L_D, L_E, L_TAU, L_PV, L_Y, L_DS, L_ZS, L_PERM, L_ACT, L_RCS,
   L_SLOT, L_END, L_K, L_DND, L_ZND, L_ORG, L_TAUS, L_ZH, L_RHO, L_MG, L_LEAF, L_GD, L_FAIL, L_YB,
-  L_T, L_W1, L_W2, L_YTY, L_NUM
+  L_T, L_W1, L_W2, L_YTY, L_PART, L_SPLIT, L_NUM
 };
 
 static void layout(int64_t n, size_t* off, size_t& total) {
@@ -1017,7 +1397,7 @@ static void layout(int64_t n, size_t* off, size_t& total) {
       nn * 8,                        // Qa
       nn * 8,                        // Qs
       nn * 8,                        // Sv
-      (size_t)n * 2 * kNB * 16,      // VW
+      (size_t)n * 3 * kNB * 16,      // VW (V, W, and V again for the fused update)
       (size_t)n * 8,                 // d
       (size_t)n * 8,                 // e
       (size_t)n * 16,                // tau
@@ -1034,11 +1414,13 @@ static void layout(int64_t n, size_t* off, size_t& total) {
       (size_t)n * 8,                                // leaves (lo, n)
       (size_t)n * sizeof(GemmDesc),                 // descs
       64,                                           // fail
-      (size_t)n * kNB * 16,                         // Ybuf
-      (size_t)kNB * kNB * 16,                       // T
-      (size_t)n * kNB * 16,                         // W1
-      (size_t)n * kNB * 16,                         // W2
-      (size_t)kNB * kNB * 16,                       // YtY
+      (size_t)n * kNBT * 16,                        // Ybuf
+      (size_t)kNBT * kNBT * 16,                     // T
+      (size_t)n * kNBT * 16,                        // W1
+      (size_t)n * kNBT * 16,                        // W2
+      (size_t)kNBT * kNBT * 16 * kMaxSplit,         // YtY (+ split-K partials of YtY)
+      3 * (size_t)kMaxSymvBlk * kPartStride * 8,    // hetrd partial sums
+      (size_t)n * kNBT * 16 * kMaxSplit,            // split-K partials (back-transform)
   };
   size_t o = 0;
   for (int i = 0; i < L_NUM; ++i) {
@@ -1070,25 +1452,25 @@ __global__ void k_bt_pack(const zd* __restrict__ A, int64_t n, int64_t b0, int b
   }
 }
 
-// T (b x b upper, ld kNB) from tau and YtY = Y^H Y (forward, columnwise larft)
-__global__ void k_bt_larft(const zd* __restrict__ tau, int64_t b0, int b, const zd* __restrict__ YtY,
-                           zd* __restrict__ T) {
-  // T[:i, i] = -tau_i T[:i, :i] YtY[:i, i] ; sequential over i, parallel over rows
-  __shared__ zd Ts[kNB][kNB];
+// T (b x b upper, ld kNBT) from tau and YtY = Y^H Y (forward, columnwise larft):
+// T[:i, i] = -tau_i T[:i, :i] YtY[:i, i], sequential over i, parallel over rows
+__global__ void __launch_bounds__(kNBT) k_bt_larft(const zd* __restrict__ tau, int64_t b0, int b,
+                                                   const zd* __restrict__ YtY, zd* __restrict__ T) {
+  extern __shared__ zd Ts[];  // kNBT x kNBT, Ts[row * kNBT + col]
   const int t = threadIdx.x;
-  for (int e = t; e < kNB * kNB; e += blockDim.x) Ts[e % kNB][e / kNB] = mk<double>(0, 0);
+  for (int e = t; e < kNBT * kNBT; e += blockDim.x) Ts[e] = mk<double>(0, 0);
   __syncthreads();
   for (int i = 0; i < b; ++i) {
     const zd ti = tau[b0 + i];
     if (t < i) {
       zd acc = mk<double>(0, 0);
-      for (int j = t; j < i; ++j) acc = cadd(acc, cmul(Ts[t][j], YtY[j + i * kNB]));
-      Ts[t][i] = cmul(mk<double>(-ti.x, -ti.y), acc);
+      for (int j = t; j < i; ++j) acc = cadd(acc, cmul(Ts[t * kNBT + j], YtY[j + i * kNBT]));
+      Ts[t * kNBT + i] = cmul(mk<double>(-ti.x, -ti.y), acc);
     }
-    if (t == 0) Ts[i][i] = ti;
+    if (t == 0) Ts[i * kNBT + i] = ti;
     __syncthreads();
   }
-  for (int e = t; e < kNB * kNB; e += blockDim.x) T[e] = Ts[e % kNB][e / kNB];
+  for (int e = t; e < kNBT * kNBT; e += blockDim.x) T[e] = Ts[(e % kNBT) * kNBT + e / kNBT];
 }
 
 __global__ void k_real_to_cx(const double* __restrict__ Z, zd* __restrict__ V, int64_t n) {
@@ -1098,26 +1480,37 @@ __global__ void k_real_to_cx(const double* __restrict__ Z, zd* __restrict__ V, i
 }
 
 static void backtransform(const zd* A, const zd* tau, int64_t n, zd* V, zd* Ybuf, zd* T, zd* W1,
-                          zd* W2, zd* YtY, cudaStream_t s) {
+                          zd* W2, zd* YtY, zd* part, cudaStream_t s) {
   const int64_t nref = n - 1;
   if (nref <= 0) return;
-  const int64_t nblk = ediv(nref, kNB);
+  static bool attr = (cudaFuncSetAttribute(k_bt_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kNBT * kNBT * (int)sizeof(zd)),
+                      true);
+  (void)attr;
+  const int64_t nblk = ediv(nref, kNBT);
+  const int64_t part_cap = n * kNBT * kMaxSplit;
   for (int64_t bi = nblk - 1; bi >= 0; --bi) {
-    const int64_t b0 = bi * kNB;
-    const int b = (int)std::min<int64_t>(kNB, nref - b0);
+    const int64_t b0 = bi * kNBT;
+    const int b = (int)std::min<int64_t>(kNBT, nref - b0);
     const int64_t L = n - b0 - 1;
     {
+      EigScope sc(ES_BT, s, 16.0 * (double)(L * b), 0.0);
       const int blocks = (int)std::min<int64_t>(ediv(L * b, 256), 148 * 8);
       k_bt_pack<<<blocks, 256, 0, s>>>(A, n, b0, b, Ybuf);
       EIG_CHECK();
     }
-    gemm_cm<zd, zd, true, false>(ES_BT, b, b, L, 1.0, Ybuf, L, Ybuf, L, 0.0, YtY, kNB, s);
-    k_bt_larft<<<1, 64, 0, s>>>(tau, b0, b, YtY, T);
-    EIG_CHECK();
+    gemm_cm_splitk<zd, zd, true, false>(ES_BT, b, b, L, 1.0, Ybuf, L, Ybuf, L, 0.0, YtY, kNBT,
+                                        YtY + kNBT * kNBT, kNBT * kNBT * (kMaxSplit - 1), s);
+    {
+      EigScope sc(ES_BT, s, 16.0 * kNBT * kNBT * 2.0, 8.0 * b * b * b / 3.0);
+      k_bt_larft<<<1, kNBT, kNBT * kNBT * sizeof(zd), s>>>(tau, b0, b, YtY, T);
+      EIG_CHECK();
+    }
     zd* Vs = V + (b0 + 1);
-    gemm_cm<zd, zd, true, false>(ES_BT, b, n, L, 1.0, Ybuf, L, Vs, n, 0.0, W1, kNB, s);
-    gemm_cm<zd, zd, false, false>(ES_BT, b, n, b, 1.0, T, kNB, W1, kNB, 0.0, W2, kNB, s);
-    gemm_cm<zd, zd, false, false>(ES_BT, L, n, b, -1.0, Ybuf, L, W2, kNB, 1.0, Vs, n, s);
+    gemm_cm_splitk<zd, zd, true, false>(ES_BT, b, n, L, 1.0, Ybuf, L, Vs, n, 0.0, W1, kNBT, part,
+                                        part_cap, s);
+    gemm_cm<zd, zd, false, false>(ES_BT, b, n, b, 1.0, T, kNBT, W1, kNBT, 0.0, W2, kNBT, s);
+    gemm_cm<zd, zd, false, false>(ES_BT, L, n, b, -1.0, Ybuf, L, W2, kNBT, 1.0, Vs, n, s);
   }
 }
 
@@ -1166,7 +1559,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
 
   // 2. tridiagonalize
   dbg_check("gram", G, 2 * n * n, s);
-  hetrd(G, n, VW, d, e, tau, pv, y, s);
+  hetrd(G, n, VW, d, e, tau, pv, y, (double*)(B + off[L_PART]), s);
   dbg_check("d", d, n, s);
   dbg_check("e", e, n - 1, s);
 
@@ -1237,7 +1630,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
       EIG_CHECK();
       dim3 g((unsigned)ediv(mmax, TBM), (unsigned)ediv(mmax, TBN), (unsigned)nm);
       GemmDesc none{};
-      k_gemm_cm<double, double, false, false, 16><<<g, 256, 0, s>>>(gd, none, 1.0, 0.0);
+      k_gemm_cm<double, double, false, false, 16><<<g, 256, 0, s>>>(gd, none, 1.0, 0.0, 0);
       EIG_CHECK();
     }
     {
@@ -1262,7 +1655,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
   }
   dbg_check("VcZ", Vc, 2 * n * n, s);
   backtransform(G, tau, n, Vc, (zd*)(B + off[L_YB]), (zd*)(B + off[L_T]), (zd*)(B + off[L_W1]),
-                (zd*)(B + off[L_W2]), (zd*)(B + off[L_YTY]), s);
+                (zd*)(B + off[L_W2]), (zd*)(B + off[L_YTY]), (zd*)(B + off[L_SPLIT]), s);
   if (fail_host) {
     cudaMemcpyAsync(fail_host, fail, sizeof(int), cudaMemcpyDeviceToHost, s);
   }
@@ -1304,7 +1697,7 @@ __global__ void k_cvt_v(const zd* __restrict__ Vc, cx<R>* __restrict__ V, int64_
 }
 
 bool gram_path_ok(int64_t p, double eps) {
-  static const int64_t min_p = getenv("MB_GRAM_MIN_P") ? atoll(getenv("MB_GRAM_MIN_P")) : 256;
+  static const int64_t min_p = getenv("MB_GRAM_MIN_P") ? atoll(getenv("MB_GRAM_MIN_P")) : 512;
   if (min_p <= 0 || p < min_p) return false;
   // the weight budget eps^2 |A|^2 must sit far above the Gram's resolution
   // p u |A|^2 (u = fp64 unit roundoff)
@@ -1315,6 +1708,46 @@ template <typename R>
 size_t gram_workspace_bytes(int64_t m, int64_t n) {
   const int64_t p = m < n ? m : n;
   return eig_workspace_bytes(p);
+}
+
+// Is the Gram already diagonal under the Jacobi path's rotation criterion
+// (|g_jk| <= tol sqrt(g_jj g_kk) or below the backward-stability floor
+// 16 u |A|_F max(|x_j|, |x_k|), u the job precision)? Canonical-form sites
+// arrive with orthogonal columns; they then skip the eigensolver entirely.
+__global__ void k_gram_trace(const zd* __restrict__ G, int64_t p, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0;
+  for (int64_t c = threadIdx.x; c < p; c += blockDim.x) acc += G[c + c * p].x;
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) out[0] = acc;
+}
+
+__global__ void k_gram_offdiag(const zd* __restrict__ G, int64_t p, double tol, double floor_u,
+                               const double* __restrict__ trace, int* __restrict__ flag) {
+  const double fro = sqrt(fmax(trace[0], 0.0));
+  int open = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % p, c = e / p;
+    if (r >= c) continue;
+    const zd g = G[e];
+    const double a = sqrt(g.x * g.x + g.y * g.y);
+    const double gr = G[r + r * p].x, gc = G[c + c * p].x;
+    const double xmax = sqrt(fmax(fmax(gr, gc), 0.0));
+    if (a > tol * sqrt(fmax(gr, 0.0) * fmax(gc, 0.0)) && a > floor_u * fro * xmax) open = 1;
+  }
+  if (__syncthreads_or(open) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename R>
+__global__ void k_gram_diag_exit(const zd* __restrict__ G, int64_t p, R* __restrict__ sig,
+                                 cx<R>* __restrict__ V) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % p, c = e / p;
+    if (V) V[e] = mk<R>(r == c ? 1 : 0, 0);
+    if (r == c) sig[c] = (R)sqrt(fmax(G[e].x, 0.0));
+  }
 }
 
 template <typename R>
@@ -1333,6 +1766,32 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
   }
   // 1. G = X^H X in fp64
   gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s);
+  {
+    // already orthogonal columns: V = I, sigma = column norms (one read-back)
+    static thread_local int* h_flag = nullptr;
+    if (!h_flag) cudaMallocHost(&h_flag, sizeof(int));
+    int* d_flag = (int*)(B + off[L_FAIL]) + 1;
+    double* d_tr = (double*)(B + off[L_RHO]);
+    EigScope sc(ES_GRAM, s, 16.0 * (double)(p * p), 0.0);
+    cudaMemsetAsync(d_flag, 0, sizeof(int), s);
+    k_gram_trace<<<1, 1024, 0, s>>>(G, p, d_tr);
+    EIG_CHECK();
+    const double su = std::sqrt((double)std::max<int64_t>(q, 1));
+    const double tol = std::max(su, 8.0) * 4.0 * (sizeof(R) == sizeof(double) ? 1.1102230246251565e-16
+                                                                              : 5.9604644775390625e-08);
+    const double fl = 16.0 * (sizeof(R) == sizeof(double) ? 1.1102230246251565e-16 : 5.9604644775390625e-08);
+    k_gram_offdiag<<<(int)std::min<int64_t>(ediv(p * p, 256), 148 * 8), 256, 0, s>>>(G, p, tol, fl,
+                                                                                      d_tr, d_flag);
+    EIG_CHECK();
+    cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (*h_flag == 0) {
+      k_gram_diag_exit<R><<<(int)std::min<int64_t>(ediv(p * p, 256), 148 * 8), 256, 0, s>>>(
+          G, p, J.sig + p, J.V);
+      EIG_CHECK();
+      return;  // J.X already holds Y = X I
+    }
+  }
   // 2-4. eigenvectors of G
   heevd(p, ws, s, nullptr);
   // 5. V in the job precision, Y = X V, sigma = column norms of Y

@@ -240,7 +240,7 @@ static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64
                 ws, E.stream);
     return;
   }
-  static FILE* log = getenv("MB_GEMM_LOG") ? fopen(getenv("MB_GEMM_LOG"), "w") : nullptr;
+  static FILE* log = mb_debug_env("MB_GEMM_LOG") ? fopen(mb_debug_env("MB_GEMM_LOG"), "w") : nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   if (log) {  // debug: shapes and device time of the CUDA-core GEMMs
     cudaEventCreate(&t0);
@@ -285,7 +285,7 @@ static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double
 }
 
 template <typename R>
-static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n);
+static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n, long long id = -1);
 static int g_tag = 0;  // debug (MB_SVD_LOG): which engine operation issued the SVD
 
 template <typename R>
@@ -305,7 +305,7 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       double p = (double)(j.m < j.n ? j.m : j.n), q = (double)(j.m < j.n ? j.n : j.m);
       fl += 2.0 * 8.0 * p * p * q;  // one Gram + one rotation pass (lower bound)
     }
-    static FILE* log = getenv("MB_SVD_LOG") ? fopen(getenv("MB_SVD_LOG"), "w") : nullptr;
+    static FILE* log = mb_debug_env("MB_SVD_LOG") ? fopen(mb_debug_env("MB_SVD_LOG"), "w") : nullptr;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (log) {
       cudaEventCreate(&t0);
@@ -334,9 +334,25 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
   }
   for (int i = 0; i < nj; ++i) {
     int64_t p = jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n;
-    if (p > kSmallP && gram_path_ok(p, jobs[i].eps)) {
+    if (p <= kSmallP) continue;
+    // debug (MB_RANK_LOG / MB_DUMP_LARGE_INDEX): one sequence over every
+    // large job of the process, either path
+    static FILE* rlog = mb_debug_env("MB_RANK_LOG") ? fopen(mb_debug_env("MB_RANK_LOG"), "w") : nullptr;
+    static const long long dump_at =
+        mb_debug_env("MB_DUMP_LARGE_INDEX") ? atoll(mb_debug_env("MB_DUMP_LARGE_INDEX")) : -1;
+    static long long seq = 0;
+    static long long dump_lo = -1, dump_hi = -1;
+    static bool dump_init = false;
+    if (!dump_init) {
+      dump_init = true;
+      if (const char* r = mb_debug_env("MB_DUMP_RANGE")) sscanf(r, "%lld:%lld", &dump_lo, &dump_hi);
+    }
+    if (jobs[i].A && (seq == dump_at || (seq >= dump_lo && seq < dump_hi && p <= 2048)))
+      dump_matrix<R>("large", jobs[i].A, jobs[i].m, jobs[i].n, seq);
+    const bool gram = gram_path_ok(p, jobs[i].eps);
+    const double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m), pd = (double)p;
+    if (gram) {
       // truncated / values-only: fp64 Gram eigenproblem (mb_eig.cu)
-      const double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m), pd = (double)p;
       ProfScope ps(P_SVD_LARGE, 8.0 * q * pd * pd * 2.0 + (16.0 / 3.0 + 8.0 + 2.0) * pd * pd * pd);
       void* ws = grow(E.eigws, eig_workspace_bytes(p));
       if (!jobs[i].W)  // values-only batch jobs: Y and V in shared scratch
@@ -344,14 +360,11 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
                                  large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
       svd_gram<R>(jobs[i], ws, E.stream);
       finish_large<R>(jobs[i], 1, 0, E.stream);
-      E.counters[1]++;
-      continue;
-    }
-    if (p > kSmallP) {
-      double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m);
-      ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * (double)p * (double)p * q);
+    } else {
+      // exact splits and tight cutoffs: block one-sided Jacobi
+      ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * pd * pd * q);
       double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
-      const int64_t cap = large_pair_capacity(jobs[i].m < jobs[i].n ? jobs[i].m : jobs[i].n);
+      const int64_t cap = large_pair_capacity(p);
       if (E.h_lg_cap < cap) {
         if (E.h_lg) {
           ck(cudaStreamSynchronize(E.stream), "sync");
@@ -363,20 +376,21 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       int* lg = (int*)grow(E.lg_dev, sizeof(int) * 3 * cap);
       LargeScratch ws{reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, lg, E.h_lg, lg + cap,
                       E.h_lg + cap};
-      static FILE* llog = getenv("MB_SVD_LOG") ? fopen((std::string(getenv("MB_SVD_LOG")) + ".large").c_str(), "w") : nullptr;
-      auto w0 = std::chrono::steady_clock::now();
       svd_large<R>(jobs[i], ws, E.stream);
-      if (llog) {  // debug: shapes, sweeps and host wall time of the large path
-        cudaStreamSynchronize(E.stream);
-        double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
-        int64_t info[3];
-        cudaMemcpy(info, jobs[i].info, sizeof(info), cudaMemcpyDeviceToHost);
-        fprintf(llog, "%d %lld %lld %lld %lld %.1f\n", g_tag, (long long)jobs[i].m,
-                (long long)jobs[i].n, (long long)info[2], (long long)info[0], us);
-      }
-      E.counters[1]++;
       E.counters[3]++;
     }
+    E.counters[1]++;
+    if (rlog) {
+      int64_t info[3];
+      double disc = 0;
+      cudaStreamSynchronize(E.stream);
+      cudaMemcpy(info, jobs[i].info, sizeof(info), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&disc, jobs[i].disc, sizeof(double), cudaMemcpyDeviceToHost);
+      fprintf(rlog, "%lld %d %c %lld %lld %lld %.17g %g\n", seq, g_tag, gram ? 'G' : 'J',
+              (long long)jobs[i].m, (long long)jobs[i].n, (long long)info[0], disc, jobs[i].eps);
+      fflush(rlog);
+    }
+    ++seq;
   }
 }
 
@@ -423,7 +437,7 @@ static double norm_of(const cx<R>* buf, int64_t n) {
 // Debug aid (MB_CHECK_SITES=1): report the first operation whose output site
 // is all-zero or non-finite.
 static bool check_sites_enabled() {
-  static const bool on = getenv("MB_CHECK_SITES") && atoi(getenv("MB_CHECK_SITES"));
+  static const bool on = mb_debug_env("MB_CHECK_SITES") && atoi(mb_debug_env("MB_CHECK_SITES"));
   return on;
 }
 
@@ -441,10 +455,10 @@ static bool check_site(const char* op, int i, const Site& s, int d, int64_t m, i
 
 // dump a device matrix (complex) as raw complex128 for offline replay
 template <typename R>
-static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n) {
-  const char* dir = getenv("MB_DUMP_DIR");
+static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n, long long id) {
+  const char* dir = mb_debug_env("MB_DUMP_DIR");
   static int count = 0;
-  if (!dir || count >= 4) return;
+  if (!dir || (id < 0 && count >= 4)) return;
   std::vector<double> host((size_t)(2 * m * n));
   cx<double>* tmp = nullptr;
   cudaMalloc(&tmp, (size_t)(m * n) * 16);
@@ -453,8 +467,9 @@ static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n)
   cudaStreamSynchronize(E.stream);
   cudaFree(tmp);
   char path[512];
-  snprintf(path, sizeof(path), "%s/%s_%d_%lldx%lld.bin", dir, tag, count++, (long long)m,
-           (long long)n);
+  snprintf(path, sizeof(path), "%s/%s_%lld_%lldx%lld.bin", dir, tag,
+           id >= 0 ? id : (long long)count, (long long)m, (long long)n);
+  ++count;
   FILE* f = fopen(path, "wb");
   if (f) {
     fwrite(host.data(), sizeof(double), host.size(), f);
@@ -464,25 +479,6 @@ static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n)
 
 // Center moves through the explicit-Q Householder kernels (2p launches) are
 // opt-in (MB_QR_STEPS=1); by default they use the SVD split (same shapes).
-static bool use_qr_steps() {
-  static const bool on = getenv("MB_QR_STEPS") && atoi(getenv("MB_QR_STEPS"));
-  return on;
-}
-
-// QR step of A (m x n row-major). right (push_right, m >= n): A = Q R, site = Q
-// (m x n), carry = R (n x n). left (push_left, m <= n): A^H = Q R, A = R^H Q^H,
-// site = Q^H (m x n, orthonormal rows), carry = L = R^H (m x m).
-template <typename R>
-static void qr_step(const cx<R>* A, int64_t m, int64_t n, bool right, cx<R>* site, cx<R>* carry) {
-  const int64_t p = right ? n : m, q = right ? m : n;
-  cx<R>* X = (cx<R>*)grow(E.X[0], (size_t)(p * q) * sizeof(cx<R>));
-  cx<R>* Y = (cx<R>*)grow(E.W[0], (size_t)(p * q + p) * sizeof(cx<R>));
-  ProfScope ps(P_SVD_LARGE, 8.0 * 2.0 * (double)q * (double)p * (double)p);
-  launch_to_x<R>(A, X, m, n, !right, E.stream);
-  qr_explicit<R>(X, Y, Y + p * q, q, p, E.stream);
-  launch_qr_emit<R>(Y, X, q, p, right, site, carry, E.stream);
-}
-
 // Left-orthogonalize site i, pushing the remainder into site i+1 (chains.py:110).
 template <typename R>
 static void push_right(mb_chain& c, int i) {
@@ -498,12 +494,6 @@ static void push_right(mb_chain& c, int i) {
     }
     nB = new_site<R>(m, d, B.r);
     gemm<R>(false, m, rn, n, P<R>(A), n, P<R>(B), rn, P<R>(nB), rn);
-  } else if (n > kSmallP && use_qr_steps()) {  // Householder QR (chains.py:113)
-    nA = new_site<R>(A.l, d, n);
-    cx<R>* Rm = (cx<R>*)grow(E.carry, (size_t)(n * n) * sizeof(cx<R>));
-    qr_step<R>(P<R>(A), m, n, true, P<R>(nA), Rm);
-    nB = new_site<R>(n, d, B.r);
-    gemm<R>(false, n, rn, n, Rm, n, P<R>(B), rn, P<R>(nB), rn);
   } else {
     g_tag = 1;
     SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
@@ -535,12 +525,6 @@ static void push_left(mb_chain& c, int i) {
     }
     nP = new_site<R>(Pv.l, d, n);
     gemm<R>(false, pm, n, m, P<R>(Pv), m, P<R>(A), n, P<R>(nP), n);
-  } else if (m > kSmallP && use_qr_steps()) {  // LQ via Householder QR of A^H (chains.py:123)
-    nA = new_site<R>(m, d, A.r);
-    cx<R>* L = (cx<R>*)grow(E.carry, (size_t)(m * m) * sizeof(cx<R>));
-    qr_step<R>(P<R>(A), m, n, false, P<R>(nA), L);
-    nP = new_site<R>(Pv.l, d, m);
-    gemm<R>(false, pm, m, m, P<R>(Pv), m, L, m, P<R>(nP), m);
   } else {
     g_tag = 2;
     SvdJob<R> j = make_job<R>(0, P<R>(A), m, n, 0.0, std::numeric_limits<int64_t>::max(), true);
@@ -586,7 +570,6 @@ static bool fuse_right(const mb_chain& c, int i) {
   const Site &A = c.s[i], &B = c.s[i + 1];
   const int64_t m = A.l * c.d, n = A.r, rn = (int64_t)c.d * B.r;
   if (m < n) return m * rn * n <= kSweepGemmMax;
-  if (n > kSmallP && use_qr_steps()) return false;
   return fuse_svd(m, n) && n * rn * n <= kSweepGemmMax;
 }
 
@@ -595,7 +578,6 @@ static bool fuse_left(const mb_chain& c, int i) {
   const Site &A = c.s[i], &Pv = c.s[i - 1];
   const int64_t m = A.l, n = (int64_t)c.d * A.r, pm = Pv.l * c.d;
   if (m > n) return pm * n * m <= kSweepGemmMax;
-  if (m > kSmallP && use_qr_steps()) return false;
   return fuse_svd(m, n) && pm * m * m <= kSweepGemmMax;
 }
 
@@ -622,7 +604,7 @@ static void sweep_launch(SweepPack<R>& pk, int64_t max_pq, int64_t max_pp) {
   pk.carry = (cx<R>*)grow(E.sw_carry, (size_t)std::max<int64_t>(max_pq, 1) * sizeof(cx<R>));
   double fl = 0;
   for (int t = 0; t < pk.n; ++t) fl += 8.0 * pk.st[t].l * pk.st[t].r;  // nominal
-  static FILE* log = getenv("MB_SVD_LOG") ? fopen((std::string(getenv("MB_SVD_LOG")) + ".sweep").c_str(), "w") : nullptr;
+  static FILE* log = mb_debug_env("MB_SVD_LOG") ? fopen((std::string(mb_debug_env("MB_SVD_LOG")) + ".sweep").c_str(), "w") : nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   if (log) {
     cudaEventCreate(&t0);
@@ -855,7 +837,7 @@ static int try_bond(mb_chain& c, int b, int ns, const int* sides, double eps, in
   require(c.d == 4, "swap on a non-operator chain");
   require(b >= 0 && b + 1 < c.n, "bond out of range");
   require(ns >= 0 && ns <= 3, "0..3 sides");
-  static FILE* tlog = getenv("MB_TRYBOND_LOG") ? fopen(getenv("MB_TRYBOND_LOG"), "w") : nullptr;
+  static FILE* tlog = mb_debug_env("MB_TRYBOND_LOG") ? fopen(mb_debug_env("MB_TRYBOND_LOG"), "w") : nullptr;
   double tm[4] = {0, 0, 0, 0};
   auto tick = std::chrono::steady_clock::now();
   auto mark = [&](int i) {  // debug: host wall per phase (synchronizing)
@@ -1449,7 +1431,7 @@ static void init_context(int device) {
 template <typename R>
 static void trial(mb_chain& c, int ng, const int* kinds, const int* qubits, const double* mats,
                   int side, double eps, int64_t chi) {
-  static FILE* log = getenv("MB_TRIAL_LOG") ? fopen(getenv("MB_TRIAL_LOG"), "w") : nullptr;
+  static FILE* log = mb_debug_env("MB_TRIAL_LOG") ? fopen(mb_debug_env("MB_TRIAL_LOG"), "w") : nullptr;
   static std::mutex log_mu;
   auto t0 = std::chrono::steady_clock::now();
   int n2 = 0;

@@ -1619,216 +1619,6 @@ __global__ void k_rank(SvdJob<R> J, int64_t p, int conv, int sweeps) {
   }
 }
 
-// ---- QR preconditioning (zgejsv-style) -----------------------------------
-// X0 (q x p, column-major) = Q R by Householder reflections (zgeqrf
-// conventions: v below the diagonal with implicit 1, beta on the diagonal).
-// One launch per column: every CTA owns whole trailing columns, forms
-// w_j = v^H x_j and x_j -= conj(tau) v w_j; the CTA that owns column k+1 then
-// builds the next reflector (look-ahead), so launch k+1 finds it ready.
-
-template <typename R>
-__device__ void make_reflector(cx<R>* __restrict__ col, int64_t k, int64_t q, cx<R>* tau_out,
-                               double* red) {
-  // col points at column k; rows k..q-1 are live. All magnitudes are scaled by
-  // the column's max-abs entry so that rank-deficient trailing columns (pure
-  // rounding noise that shrinks toward the underflow range) never produce a
-  // zero denominator (zlarfg's rescaling, done once by the max-abs scale).
-  double mx = 0;
-  for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
-    cx<R> v = col[r];
-    mx = fmax(mx, fmax(fabs((double)v.x), fabs((double)v.y)));
-  }
-  red[threadIdx.x] = mx;
-  __syncthreads();
-  for (int sft = blockDim.x / 2; sft > 0; sft >>= 1) {
-    if (threadIdx.x < sft) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + sft]);
-    __syncthreads();
-  }
-  const double amax = red[0];
-  __syncthreads();
-  // Columns below the safe minimum are rounding noise that has decayed through
-  // the trailing reflections (down to denormals); 1/amax would overflow, and
-  // H = I is exact to that precision.
-  const double safmin = sizeof(R) == sizeof(double) ? 1e-150 : 1e-18;
-  if (!(amax > safmin)) {
-    if (threadIdx.x == 0) *tau_out = mk<R>(0, 0);
-    return;
-  }
-  const double inv = 1.0 / amax;
-  double acc = 0;
-  for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) {
-    cx<R> v = col[r];
-    double a = v.x * inv, b = v.y * inv;
-    acc += a * a + b * b;
-  }
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int sft = blockDim.x / 2; sft > 0; sft >>= 1) {
-    if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
-    __syncthreads();
-  }
-  const double xn2 = red[0];  // scaled
-  const cx<R> alpha = col[k];
-  __syncthreads();
-  if (xn2 == 0.0 && alpha.y == 0) {
-    if (threadIdx.x == 0) *tau_out = mk<R>(0, 0);
-    return;
-  }
-  const double ar = alpha.x * inv, ai = alpha.y * inv;  // scaled alpha
-  const double an = sqrt(ar * ar + ai * ai + xn2);      // scaled |(alpha, x)|
-  const double bs = ar >= 0 ? -an : an;                 // scaled beta
-  // tau = (beta - alpha) / beta (scale-free) ; 1 / (alpha - beta) = inv / (a_s - b_s)
-  const double dr = ar - bs, di = ai;
-  const double den = dr * dr + di * di;  // >= an^2 >= ~1 in scaled units
-  const cx<R> scale = mk<R>((R)(inv * dr / den), (R)(-inv * di / den));
-  for (int64_t r = k + 1 + threadIdx.x; r < q; r += blockDim.x) col[r] = cmul(col[r], scale);
-  if (threadIdx.x == 0) {
-    *tau_out = mk<R>((R)((bs - ar) / bs), (R)(-ai / bs));
-    col[k] = mk<R>((R)(bs * amax), 0);
-  }
-}
-
-template <typename R>
-__global__ void __launch_bounds__(256) k_qr_first(cx<R>* __restrict__ X, int64_t q,
-                                                 cx<R>* __restrict__ tau) {
-  __shared__ double red[256];
-  make_reflector<R>(X, 0, q, &tau[0], red);
-}
-
-// apply reflector k to columns k+1.. (each CTA: a strided set of columns)
-template <typename R>
-__global__ void __launch_bounds__(256) k_qr_step(cx<R>* __restrict__ X, int64_t q, int64_t p,
-                                                int64_t k, cx<R>* __restrict__ tau) {
-  __shared__ double red[256];
-  __shared__ cx<R> wj;
-  const cx<R> tk = tau[k];
-  const cx<R>* v = X + k * q;  // v[k] = 1 implicitly
-  for (int64_t j = k + 1 + blockIdx.x; j < p; j += gridDim.x) {
-    cx<R>* x = X + j * q;
-    if (!(tk.x == 0 && tk.y == 0)) {
-      // w = v^H x over rows k..q-1
-      double ax = 0, ay = 0;
-      for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
-        cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
-        cx<R> xr = x[r];
-        ax += (double)vr.x * xr.x + (double)vr.y * xr.y;
-        ay += (double)vr.x * xr.y - (double)vr.y * xr.x;
-      }
-      red[threadIdx.x] = ax;
-      __syncthreads();
-      for (int sft = 128; sft > 0; sft >>= 1) {
-        if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) wj.x = (R)red[0];
-      __syncthreads();
-      red[threadIdx.x] = ay;
-      __syncthreads();
-      for (int sft = 128; sft > 0; sft >>= 1) {
-        if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) wj.y = (R)red[0];
-      __syncthreads();
-      // x -= conj(tau) * v * w
-      const cx<R> f = cmul(cconj(tk), wj);
-      for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
-        cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
-        x[r] = csub(x[r], cmul(vr, f));
-      }
-      __syncthreads();
-    }
-    if (j == k + 1) make_reflector<R>(x, j, q, &tau[j], red);
-    __syncthreads();
-  }
-}
-
-// Z = R^H (p x p, column-major, lower triangular) from the QR'd X
-template <typename R>
-__global__ void k_make_z(const cx<R>* __restrict__ X, int64_t q, int64_t p, cx<R>* __restrict__ Z) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t j = e / p, i = e % p;  // Z(i, j) = conj(R(j, i)), R(j, i) = X[i*q + j] for j <= i
-    Z[e] = j <= i ? cconj(X[i * q + j]) : mk<R>(0, 0);
-  }
-}
-
-// U~ = Z' diag(1/sigma) (unsorted columns; zero-safe)
-template <typename R>
-__global__ void k_scale_cols(const cx<R>* __restrict__ Zr, const R* __restrict__ nrm, int64_t p,
-                             cx<R>* __restrict__ out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    R s = nrm[e / p];
-    out[e] = s > 0 ? cscale(Zr[e], (R)1 / s) : mk<R>(0, 0);
-  }
-}
-
-// Explicit Q (q x p, column-major) by backward accumulation:
-// Y = [I; 0]; for k = p-1..0: Y[k:, k:] <- H_k Y[k:, k:], H_k = I - tau v v^H.
-template <typename R>
-__global__ void k_q_init(cx<R>* __restrict__ Y, int64_t q, int64_t p) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < q * p;
-       e += (int64_t)gridDim.x * blockDim.x)
-    Y[e] = mk<R>((e % q) == (e / q) ? 1 : 0, 0);
-}
-
-template <typename R>
-__global__ void __launch_bounds__(256) k_q_step(const cx<R>* __restrict__ X, cx<R>* __restrict__ Y,
-                                               int64_t q, int64_t p, int64_t k,
-                                               const cx<R>* __restrict__ tau) {
-  __shared__ double red[2][256];
-  const cx<R> tk = tau[k];
-  if (tk.x == 0 && tk.y == 0) return;
-  const cx<R>* v = X + k * q;
-  for (int64_t j = k + blockIdx.x; j < p; j += gridDim.x) {
-    cx<R>* y = Y + j * q;
-    double ax = 0, ay = 0;
-    for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
-      cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
-      cx<R> yr = y[r];
-      ax += (double)vr.x * yr.x + (double)vr.y * yr.y;
-      ay += (double)vr.x * yr.y - (double)vr.y * yr.x;
-    }
-    red[0][threadIdx.x] = ax;
-    red[1][threadIdx.x] = ay;
-    __syncthreads();
-    for (int sft = 128; sft > 0; sft >>= 1) {
-      if (threadIdx.x < sft) {
-        red[0][threadIdx.x] += red[0][threadIdx.x + sft];
-        red[1][threadIdx.x] += red[1][threadIdx.x + sft];
-      }
-      __syncthreads();
-    }
-    const cx<R> f = cmul(tk, mk<R>((R)red[0][0], (R)red[1][0]));
-    for (int64_t r = k + threadIdx.x; r < q; r += blockDim.x) {
-      cx<R> vr = r == k ? mk<R>(1, 0) : v[r];
-      y[r] = csub(y[r], cmul(vr, f));
-    }
-    __syncthreads();
-  }
-}
-
-// Householder QR of the column-major X (q x p, q >= p) in place (R in the
-// upper triangle, reflectors below) plus explicit Q into Y (q x p).
-template <typename R>
-void qr_explicit(cx<R>* X, cx<R>* Y, cx<R>* tau, int64_t q, int64_t p, cudaStream_t s) {
-  k_qr_first<R><<<1, 256, 0, s>>>(X, q, tau);
-  MB_LAUNCH_CHECK();
-  for (int64_t k = 0; k + 1 < p; ++k) {
-    int g = (int)std::min<int64_t>(p - k - 1, 148 * 4);
-    k_qr_step<R><<<g, 256, 0, s>>>(X, q, p, k, tau);
-    MB_LAUNCH_CHECK();
-  }
-  int blocks = (int)std::min<int64_t>(cdiv(q * p, 256), 148 * 16);
-  k_q_init<R><<<blocks, 256, 0, s>>>(Y, q, p);
-  MB_LAUNCH_CHECK();
-  for (int64_t k = p - 1; k >= 0; --k) {
-    int g = (int)std::min<int64_t>(p - k, 148 * 4);
-    k_q_step<R><<<g, 256, 0, s>>>(X, Y, q, p, k, tau);
-    MB_LAUNCH_CHECK();
-  }
-}
 
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n) {
@@ -1865,8 +1655,8 @@ struct PhaseLog {
   std::chrono::steady_clock::time_point t;
   cudaStream_t s;
   explicit PhaseLog(cudaStream_t st) : s(st) {
-    static FILE* g = getenv("MB_SVD_LOG")
-                         ? fopen((std::string(getenv("MB_SVD_LOG")) + ".phase").c_str(), "w")
+    static FILE* g = mb_debug_env("MB_SVD_LOG")
+                         ? fopen((std::string(mb_debug_env("MB_SVD_LOG")) + ".phase").c_str(), "w")
                          : nullptr;
     f = g;
     if (f) {
@@ -1902,7 +1692,7 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const La
                           R* colnorm) {
   static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : (env_int("MB_JACOBI_W2", 32) == 16 ? 16 : 32);
   static const int inner = env_int("MB_JACOBI_INNER", 1);
-  static const int debug = env_int("MB_JACOBI_DEBUG", 0);
+  static const int debug = (MB_DEBUG_LOGS && env_int("MB_JACOBI_DEBUG", 0));
   static const int dynamic = env_int("MB_JACOBI_DYNAMIC", 1);
   const int w = W2 / 2;
   // ||Xw||_F^2 (rotation-invariant) for the backward-stability floor: block
@@ -1995,30 +1785,6 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const La
   }
 }
 
-template <typename R>
-__global__ void k_count_bad(const cx<R>* __restrict__ x, int64_t n, int* out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    cx<R> v = x[e];
-    if (!isfinite((double)v.x) || !isfinite((double)v.y)) atomicAdd(out, 1);
-  }
-}
-
-// MB_CHECK_SITES debug aid: count non-finite entries of a device buffer
-template <typename R>
-static int count_bad(const cx<R>* x, int64_t n, cudaStream_t s) {
-  static int* d = nullptr;
-  static int* h = nullptr;
-  if (!d) {
-    cudaMalloc(&d, sizeof(int));
-    cudaMallocHost(&h, sizeof(int));
-  }
-  cudaMemsetAsync(d, 0, sizeof(int), s);
-  k_count_bad<R><<<148, 256, 0, s>>>(x, n, d);
-  cudaMemcpyAsync(h, d, sizeof(int), cudaMemcpyDeviceToHost, s);
-  cudaStreamSynchronize(s);
-  return *h;
-}
 
 // Test hook (mb_debug_fail_svd): the next n large-path convergence outcomes
 // are reported as failures, to exercise the perturbed retry and the error.
@@ -2076,147 +1842,33 @@ void finish_large(SvdJob<R>& J, int conv, int sweeps, cudaStream_t s) {
 
 template <typename R>
 void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
-  static const int dbg = env_int("MB_CHECK_SITES", 0);
-  // QR preconditioning is used for values-only problems and for truncations at
-  // cutoffs >= 1e-6, where every kept singular value sits far above the noise
-  // floor so U~ = Z J / sigma is accurate. Tighter cutoffs (which keep
-  // noise-level columns) use the plain path, whose J is unitary by construction.
-  // Opt-in (MB_JACOBI_QR=1): on random graded matrices it cuts sweeps 3x, but on
-  // the contraction's own blobs (degenerate, permutation-like spectra) R^H
-  // converges slower than X itself (c20: 14.4k vs 3.5k sweeps), so the plain
-  // path is the default.
-  static const int allow_pre = env_int("MB_JACOBI_QR", 0);
-  const int precond = allow_pre && J.W != nullptr && (J.V == nullptr || J.eps >= 1e-6);
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   PhaseLog plog(s);
   if (J.A) {
-    k_init_large<R><<<kSumBlocks, 256, 0, s>>>(J.A, J.X, precond ? nullptr : J.V, J.m, J.n,
+    k_init_large<R><<<kSumBlocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n,
                                                ws.red_dev);
     MB_LAUNCH_CHECK();
   }
   plog.mark("init");
   int conv = 0, sweeps = 0;
-  if (!precond) {
-    // the final check launch leaves the column norms in sig[p, 2p)
-    jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps, J.A != nullptr, J.sig + p);
-    if (consume_forced_failure()) conv = 0;
-    if (!conv) {
-      // one retry on a deterministically perturbed copy (tensor.py:139-150):
-      // X V^H + delta with |delta| ~ 1e-14 |A|_F, then sweep on
-      k_perturb<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, ws.red_dev + kSumBlocks);
-      MB_LAUNCH_CHECK();
-      int sweeps2 = 0;
-      jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps2, false, J.sig + p);
-      if (consume_forced_failure()) conv = 0;
-      sweeps += sweeps2;
-    }
-    plog.mark(sweeps ? "sweeps" : "check");
-  } else {
-    // 1. X0 = Q R (Householder, in the workspace copy)
-    cx<R>* Xq = J.W;
-    cx<R>* Z = J.W + q * p;
-    cx<R>* tau = Z + p * p;
-    if (dbg) {
-      int b0 = count_bad<R>(J.A, J.m * J.n, s), b1 = count_bad<R>(J.X, q * p, s);
-      if (b0 || b1) fprintf(stderr, "[svd_large dbg] bad input A=%d X0=%d (m=%lld n=%lld)\n", b0, b1,
-                            (long long)J.m, (long long)J.n);
-    }
-    cudaMemcpyAsync(Xq, J.X, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToDevice, s);
-    k_qr_first<R><<<1, 256, 0, s>>>(Xq, q, tau);
+  // the final check launch leaves the column norms in sig[p, 2p)
+  jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps, J.A != nullptr, J.sig + p);
+  if (consume_forced_failure()) conv = 0;
+  if (!conv) {
+    // one retry on a deterministically perturbed copy (tensor.py:139-150):
+    // X V^H + delta with |delta| ~ 1e-14 |A|_F, then sweep on
+    k_perturb<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, ws.red_dev + kSumBlocks);
     MB_LAUNCH_CHECK();
-    for (int64_t k = 0; k + 1 < p; ++k) {
-      int g = (int)std::min<int64_t>(p - k - 1, 148 * 4);
-      k_qr_step<R><<<g, 256, 0, s>>>(Xq, q, p, k, tau);
-      MB_LAUNCH_CHECK();
-    }
-    // 2. Z = R^H ; one-sided Jacobi on Z (p x p) without accumulating J
-    {
-      int blocks = (int)std::min<int64_t>(cdiv(p * p, 256), 148 * 16);
-      k_make_z<R><<<blocks, 256, 0, s>>>(Xq, q, p, Z);
-      MB_LAUNCH_CHECK();
-    }
-    if (dbg) {
-      int bq = count_bad<R>(Xq, q * p, s), bt = count_bad<R>(tau, p, s), bz = count_bad<R>(Z, p * p, s);
-      if (bq || bt || bz) {
-        fprintf(stderr, "[svd_large dbg] after QR: Xq=%d tau=%d Z=%d (q=%lld p=%lld)\n", bq, bt, bz,
-                (long long)q, (long long)p);
-        const char* dir = getenv("MB_DUMP_DIR");
-        static int dumped = 0;
-        if (dir && !dumped) {
-          dumped = 1;
-          std::vector<cx<R>> h((size_t)(q * p)), hq((size_t)(q * p)), ht((size_t)p);
-          cudaMemcpy(h.data(), J.X, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToHost);
-          cudaMemcpy(hq.data(), Xq, sizeof(cx<R>) * (size_t)(q * p), cudaMemcpyDeviceToHost);
-          cudaMemcpy(ht.data(), tau, sizeof(cx<R>) * (size_t)p, cudaMemcpyDeviceToHost);
-          {
-            char pq[512];
-            snprintf(pq, sizeof(pq), "%s/xq_%lldx%lld_%d.bin", dir, (long long)q, (long long)p, (int)sizeof(R));
-            FILE* g = fopen(pq, "wb");
-            if (g) { fwrite(hq.data(), sizeof(cx<R>), hq.size(), g); fwrite(ht.data(), sizeof(cx<R>), ht.size(), g); fclose(g); }
-          }
-          char path[512];
-          snprintf(path, sizeof(path), "%s/x0_%lldx%lld_%d.bin", dir, (long long)q, (long long)p,
-                   (int)sizeof(R));
-          FILE* f = fopen(path, "wb");
-          if (f) { fwrite(h.data(), sizeof(cx<R>), h.size(), f); fclose(f); }
-        }
-      }
-    }
-    jacobi_sweeps<R>(Z, nullptr, p, p, ws, s, conv, sweeps, false, J.sig + p);
-    if (dbg) {
-      int bz = count_bad<R>(Z, p * p, s);
-      if (bz) fprintf(stderr, "[svd_large dbg] after Jacobi: Z=%d sweeps=%d\n", bz, sweeps);
-    }
-    // 3. sigma = column norms of Z J (left by the final check); U~ = Z J / sigma ; U*sigma = X0 U~
-    if (J.V) {
-      int blocks = (int)std::min<int64_t>(cdiv(p * p, 256), 148 * 16);
-      k_scale_cols<R><<<blocks, 256, 0, s>>>(Z, J.sig + p, p, J.V);
-      MB_LAUNCH_CHECK();
-      // row-major: (U sigma)^T (p x q) = U~^T (p x p) @ X0^T (p x q)
-      launch_gemm<R>(false, p, q, p, J.V, p, J.X, q, Xq, q, s);
-      J.X = Xq;
-      if (dbg) {
-        int bv = count_bad<R>(J.V, p * p, s), bx = count_bad<R>(Xq, q * p, s);
-        if (bv || bx) fprintf(stderr, "[svd_large dbg] after assembly: V=%d X=%d\n", bv, bx);
-      }
-    }
+    int sweeps2 = 0;
+    jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps2, false, J.sig + p);
+    if (consume_forced_failure()) conv = 0;
+    sweeps += sweeps2;
   }
+  plog.mark(sweeps ? "sweeps" : "check");
   finish_large<R>(J, conv, sweeps, s);
   plog.mark("sort+rank");
 }
 
-// QR-step outputs. Q (q x p col-major) / R (upper triangle of the QR'd X).
-//  tall (push_right, X = A):   site = Q as row-major (q x p); carry = R row-major (p x p)
-//  wide (push_left,  X = A^H): site = Q^H row-major (p x q);  carry = R^H row-major (p x p)
-template <typename R>
-__global__ void k_qr_emit(const cx<R>* __restrict__ Q, const cx<R>* __restrict__ Xr, int64_t q,
-                          int64_t p, bool tall, cx<R>* __restrict__ site, cx<R>* __restrict__ carry) {
-  const int64_t ns = q * p, nc = p * p;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ns + nc;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < ns) {
-      if (tall) {
-        int64_t r = e / p, c = e % p;  // site[r][c] = Q(r, c)
-        site[e] = Q[c * q + r];
-      } else {
-        int64_t r = e / q, c = e % q;  // site[r][c] = conj(Q(c, r))
-        site[e] = cconj(Q[r * q + c]);
-      }
-    } else {
-      int64_t f = e - ns, r = f / p, c = f % p;
-      if (tall) carry[f] = r <= c ? Xr[c * q + r] : mk<R>(0, 0);          // R(r, c)
-      else carry[f] = c <= r ? cconj(Xr[r * q + c]) : mk<R>(0, 0);         // conj(R(c, r))
-    }
-  }
-}
-
-template <typename R>
-void launch_qr_emit(const cx<R>* Q, const cx<R>* Xr, int64_t q, int64_t p, bool tall, cx<R>* site,
-                    cx<R>* carry, cudaStream_t s) {
-  int blocks = (int)std::min<int64_t>(cdiv(q * p + p * p, 256), 148 * 16);
-  k_qr_emit<R><<<blocks, 256, 0, s>>>(Q, Xr, q, p, tall, site, carry);
-  MB_LAUNCH_CHECK();
-}
 
 template <typename R>
 __global__ void k_to_x(const cx<R>* __restrict__ A, cx<R>* __restrict__ X, int64_t m, int64_t n,
@@ -2588,9 +2240,6 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void svd_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                     \
   template void finish_large<R>(SvdJob<R>&, int, int, cudaStream_t);                            \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
-  template void qr_explicit<R>(cx<R>*, cx<R>*, cx<R>*, int64_t, int64_t, cudaStream_t);        \
-  template void launch_qr_emit<R>(const cx<R>*, const cx<R>*, int64_t, int64_t, bool, cx<R>*,   \
-                                  cx<R>*, cudaStream_t);                                        \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
   template void launch_sweep<R>(const SweepPack<R>&, cudaStream_t);                             \
   template void launch_try_bond_small<R>(const TryBondArgs<R>&, cudaStream_t);                 \

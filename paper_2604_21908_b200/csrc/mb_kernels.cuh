@@ -161,17 +161,6 @@ void force_svd_failures(int n);
 template <typename R>
 void finish_large(SvdJob<R>& J, int conv, int sweeps, cudaStream_t s);
 
-// Householder QR (zgeqrf conventions) of the column-major X (q x p) in place,
-// explicit Q into Y; tau needs p entries.
-template <typename R>
-void qr_explicit(cx<R>* X, cx<R>* Y, cx<R>* tau, int64_t q, int64_t p, cudaStream_t s);
-
-// site/carry of a QR step from (Q, R): tall = push_right (site Q, carry R),
-// wide = push_left (site Q^H, carry R^H = L), all row-major.
-template <typename R>
-void launch_qr_emit(const cx<R>* Q, const cx<R>* Xr, int64_t q, int64_t p, bool tall, cx<R>* site,
-                    cx<R>* carry, cudaStream_t s);
-
 // A (m x n row-major) -> column-major working X: A itself (q = m) or A^H (herm, q = n)
 template <typename R>
 void launch_to_x(const cx<R>* A, cx<R>* X, int64_t m, int64_t n, bool herm, cudaStream_t s);

@@ -40,7 +40,7 @@ def _unitary(rng, n):
     return q * (np.diag(r) / np.abs(np.diag(r)))
 
 
-@pytest.mark.parametrize("n", [1, 2, 31, 33, 64, 100, 257, 600])
+@pytest.mark.parametrize("n", [1, 2, 31, 33, 64, 100, 257, 600, 1000, 1700])
 def test_herm_eig_random(n):
     rng = np.random.default_rng(n)
     a = _crandn(rng, n, n)

@@ -50,7 +50,7 @@ def main():
         tr = job.trace[-1] if job.trace else None
         print(f"t={now - t0:8.2f}s steps={job.step} consumed={job.consumed} "
               f"elements={tr.elements if tr else 0} bonds_max={max(job.m.bond_dims() or (1,))} "
-              f"unswaps={job.unswap_calls} dt={now - last:.2f}s", flush=True)
+              f"unswaps={job.unswap_calls} dt={now - last:.2f}s large={nat.counters()['svd_large']}", flush=True)
         last = now
         if a.max_steps is not None and job.step >= a.max_steps:
             break
