@@ -170,7 +170,8 @@ int mb_gemm(const double* a, const double* b, int64_t m, int64_t n, int64_t k, i
 /* Truncated SVD of a host m x n complex128 matrix computed on the device
  * (tensor.py:84-116). Writes u (m x k), s (k), v (k x n) for the kept rank k
  * (buffers sized for min(m, n)); *rank = k; *discarded = relative discarded
- * weight. */
+ * weight. u = v = NULL runs the values-only decomposition of candidate scoring
+ * (unswap.py:104-112) and fills s only. */
 int mb_svd_truncate(const double* a, int64_t m, int64_t n, int dtype, double eps, int64_t chi_max,
                     double* u, double* s, double* v, int64_t* rank, double* discarded);
 
@@ -181,8 +182,9 @@ int mb_svd_truncate(const double* a, int64_t m, int64_t n, int dtype, double eps
  * The Gram eigenproblem behind the truncated SVD of tensor.py:84-116. */
 int mb_herm_eig(const double* a, int64_t n, double* w, double* v);
 /* Test hook: the next n convergence outcomes of the large Jacobi path count
- * as failures. One failure is absorbed by the perturbed retry; two make the
- * call fail with MB_ERR_NUMERIC (SvdConvergenceError in Python), like
+ * as failures. A failure is retried twice (restart from the Gram
+ * eigenvectors, then the reference's perturbed copy); a third makes the call
+ * fail with MB_ERR_NUMERIC (SvdConvergenceError in Python), the contract of
  * _svd_with_retry (tensor.py:139-150). */
 int mb_debug_fail_svd(int n);
 

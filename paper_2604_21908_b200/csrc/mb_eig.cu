@@ -1062,6 +1062,7 @@ struct DcScratch {
 };
 
 // Deflation (one CTA per merge): z, sort, tolerance scan.
+constexpr int kDeflSmem = 12288;  // 2 x 12288 doubles = 192 KB of shared memory
 __global__ void __launch_bounds__(1024) k_dc_deflate(const DcMerge* __restrict__ mg,
                                                      const double* __restrict__ e,
                                                      double* __restrict__ D,
@@ -1070,8 +1071,11 @@ __global__ void __launch_bounds__(1024) k_dc_deflate(const DcMerge* __restrict__
   extern __shared__ double sm[];
   const DcMerge g = mg[blockIdx.x];
   const int lo = g.lo, m1 = g.m1, m = g.m1 + g.m2;
-  double* zl = sm;       // m
-  double* dlv = sm + m;  // m
+  // staging in shared memory, or (merges above kDeflSmem) in the merge's
+  // slices of the zhat / tau scratch, which are free until the secular stage
+  const bool in_smem = m <= kDeflSmem;
+  double* zl = in_smem ? sm : S.zhat + lo;      // m
+  double* dlv = in_smem ? sm + m : S.tau + lo;  // m
   const double beta = e[lo + m1 - 1];
   const double sgn = beta >= 0 ? 1.0 : -1.0;
   const double rho = 2.0 * fabs(beta);
@@ -1603,7 +1607,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
     int mmax = 0;
     for (auto& g : P.levels[h]) mmax = std::max(mmax, g.m1 + g.m2);
     {
-      const size_t sm = 2 * (size_t)mmax * sizeof(double);
+      const size_t sm = 2 * (size_t)std::min(mmax, kDeflSmem) * sizeof(double);
       static bool attr = (cudaFuncSetAttribute(k_dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                227 * 1024),
                           true);
@@ -1659,6 +1663,76 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
   if (fail_host) {
     cudaMemcpyAsync(fail_host, fail, sizeof(int), cudaMemcpyDeviceToHost, s);
   }
+}
+
+// ---- values only: bisection on the tridiagonal ---------------------------------
+//
+// Eigenvalues of the symmetric tridiagonal (d, e) by Sturm-count bisection,
+// one thread per eigenvalue (LAPACK dstebz's method, absolute accuracy
+// ~ u |T|). Candidate scoring needs only the spectrum, so it skips the
+// eigenvectors, the back-transformation and X V.
+__global__ void __launch_bounds__(256) k_bisect(const double* __restrict__ d,
+                                                const double* __restrict__ e, int64_t n,
+                                                double* __restrict__ w) {
+  __shared__ double red_lo[8], red_hi[8], red_e[8];
+  double lo = INFINITY, hi = -INFINITY, emax = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+    if (i + 1 < n) emax = fmax(emax, fabs(e[i]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red_lo[wid] = lo;
+    red_hi[wid] = hi;
+    red_e[wid] = emax;
+  }
+  __syncthreads();
+  lo = red_lo[0];
+  hi = red_hi[0];
+  emax = red_e[0];
+  for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+    lo = fmin(lo, red_lo[k]);
+    hi = fmax(hi, red_hi[k]);
+    emax = fmax(emax, red_e[k]);
+  }
+  const double span = fmax(fabs(lo), fabs(hi));
+  lo -= 2.2e-16 * span * 2 * n + 1e-300;
+  hi += 2.2e-16 * span * 2 * n + 1e-300;
+  const double pivmin = fmax(1e-290, 2.2e-16 * emax * emax * 1e-3);
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    // number of eigenvalues below mid
+    int64_t cnt = 0;
+    double q = d[0] - mid;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0;
+    for (int64_t i = 1; i < n; ++i) {
+      q = (d[i] - mid) - e[i - 1] * e[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0;
+    }
+    if (cnt > k) hi = mid;
+    else lo = mid;
+  }
+  w[k] = 0.5 * (lo + hi);
+}
+
+template <typename R>
+__global__ void k_sig_from_eig(const double* __restrict__ w, int64_t n, R* __restrict__ sig) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    sig[e] = (R)sqrt(fmax(w[e], 0.0));
 }
 
 // ---- 5. SVD assembly -------------------------------------------------------------------
@@ -1792,6 +1866,24 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
       return;  // J.X already holds Y = X I
     }
   }
+  if (!J.V) {
+    // values only: tridiagonalize, bisect, sigma = sqrt(max(lambda, 0))
+    zd* VW = (zd*)(B + off[L_VW]);
+    double* d = (double*)(B + off[L_D]);
+    double* e = (double*)(B + off[L_E]);
+    double* w = (double*)(B + off[L_DS]);
+    dbg_check("gram", G, 2 * p * p, s);
+    hetrd(G, p, VW, d, e, (zd*)(B + off[L_TAU]), (zd*)(B + off[L_PV]), (zd*)(B + off[L_Y]),
+          (double*)(B + off[L_PART]), s);
+    {
+      EigScope sc(ES_DC, s, 16.0 * (double)p, 0.0);
+      k_bisect<<<(int)ediv(p, 256), 256, 0, s>>>(d, e, p, w);
+      EIG_CHECK();
+      k_sig_from_eig<R><<<(int)std::min<int64_t>(ediv(p, 256), 148), 256, 0, s>>>(w, p, J.sig + p);
+      EIG_CHECK();
+    }
+    return;
+  }
   // 2-4. eigenvectors of G
   heevd(p, ws, s, nullptr);
   // 5. V in the job precision, Y = X V, sigma = column norms of Y
@@ -1813,6 +1905,38 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
   }
 }
 
+// Precondition a Jacobi job that failed to converge: X <- X V_G, V <- V V_G
+// with V_G the eigenvectors of X^H X (fp64); the columns of the new X are
+// orthogonal to working precision, so the sweeps that follow finish in one or
+// two passes (a direct factorization seeds the iterative one).
+template <typename R>
+void gram_precondition(SvdJob<R>& J, void* ws, cudaStream_t s) {
+  const int64_t m = J.m, n = J.n;
+  const int64_t p = m < n ? m : n, q = m < n ? n : m;
+  size_t off[L_NUM], total;
+  layout(p, off, total);
+  char* B = base_ptr(ws);
+  zd* G = (zd*)(B + off[L_G]);
+  zd* Vc = (zd*)(B + off[L_VC]);
+  gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s);
+  heevd(p, ws, s, nullptr);
+  cx<R>* VG = reinterpret_cast<cx<R>*>(J.W + q * p);
+  {
+    const int blocks = (int)std::min<int64_t>(ediv(p * p, 256), 148 * 16);
+    k_cvt_v<R><<<blocks, 256, 0, s>>>(Vc, VG, p * p);
+    EIG_CHECK();
+  }
+  gemm_cm<cx<R>, cx<R>, false, false>(ES_XV, q, p, p, 1.0, J.X, q, VG, p, 0.0, J.W, q, s);
+  J.X = J.W;
+  if (J.V) {
+    cx<R>* Vn = reinterpret_cast<cx<R>*>(Vc);  // Vc is free once VG holds it
+    gemm_cm<cx<R>, cx<R>, false, false>(ES_XV, p, p, p, 1.0, J.V, p, VG, p, 0.0, Vn, p, s);
+    cudaMemcpyAsync(J.V, Vn, sizeof(cx<R>) * (size_t)(p * p), cudaMemcpyDeviceToDevice, s);
+  }
+}
+
+template void gram_precondition<double>(SvdJob<double>&, void*, cudaStream_t);
+template void gram_precondition<float>(SvdJob<float>&, void*, cudaStream_t);
 template void svd_gram<double>(SvdJob<double>&, void*, cudaStream_t);
 template void svd_gram<float>(SvdJob<float>&, void*, cudaStream_t);
 template size_t gram_workspace_bytes<double>(int64_t, int64_t);

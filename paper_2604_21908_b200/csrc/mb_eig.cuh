@@ -36,6 +36,11 @@ size_t eig_workspace_bytes(int64_t n);
 template <typename R>
 void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s);
 
+// X <- X V_G, V <- V V_G (V_G = eigenvectors of X^H X): seeds a Jacobi job
+// that failed to converge with orthogonal columns. Needs J.W.
+template <typename R>
+void gram_precondition(SvdJob<R>& J, void* ws, cudaStream_t s);
+
 // Test entry: Hermitian eigen-decomposition of a device n x n column-major
 // complex128 matrix; w ascending, V the matching eigenvectors. Returns the
 // number of leaf QL failures (0 on success). Synchronizes the stream.

@@ -376,7 +376,20 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       int* lg = (int*)grow(E.lg_dev, sizeof(int) * 3 * cap);
       LargeScratch ws{reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, lg, E.h_lg, lg + cap,
                       E.h_lg + cap};
-      svd_large<R>(jobs[i], ws, E.stream);
+      // block Jacobi; on non-convergence: Gram-preconditioned restart (direct
+      // eigensolver seeds the sweeps), then the reference's perturbed retry
+      int sweeps = 0;
+      bool conv = jacobi_large<R>(jobs[i], ws, E.stream, true, false, sweeps);
+      if (!conv) {
+        if (!jobs[i].W)
+          jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
+                                   large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
+        gram_precondition<R>(jobs[i], grow(E.eigws, eig_workspace_bytes(p)), E.stream);
+        conv = jacobi_large<R>(jobs[i], ws, E.stream, false, false, sweeps);
+        E.counters[3]++;
+      }
+      if (!conv) conv = jacobi_large<R>(jobs[i], ws, E.stream, false, true, sweeps);
+      finish_large<R>(jobs[i], conv ? 1 : 0, sweeps, E.stream);
       E.counters[3]++;
     }
     E.counters[1]++;
@@ -1020,10 +1033,13 @@ static void batch_extents(mb_chain& c, int nb, const int* bonds, const int* mine
   Buf ddisc = alloc(sizeof(double) * (size_t)(njobs > 0 ? njobs : 1));
   for (int t = 0; t < nb; ++t) {
     base_out[t] = ext_out[t] = -1;
-    if (!mine[t]) continue;
     const int b = bonds[t];
     require(b >= 0 && b + 1 < c.n, "bond out of range");
+    // every rank walks the center through every bond of the batch, owned or
+    // not, so all replicas take the same center path and stay bit-identical;
+    // only the decompositions are sharded
     move_center<R>(c, b);
+    if (!mine[t]) continue;
     Site A = c.s[b], B = c.s[b + 1];
     const int64_t l = A.l, r = B.r, M = 4 * l, N = 4 * r, K = A.r;
     const int64_t p = M < N ? M : N, q = M < N ? N : M;
@@ -1061,9 +1077,7 @@ static void batch_extents(mb_chain& c, int nb, const int* bonds, const int* mine
       owner.push_back(2 * t + v);
     }
   }
-  // every rank ends the pass with the center on the batch's last bond, so the
-  // replicas of all ranks stay bit-identical (center moves compose exactly)
-  move_center<R>(c, bonds[nb - 1]);
+  // (the center ends on the batch's last bond on every rank)
   if (jobs.empty()) return;
   run_jobs<R>(jobs.data(), (int)jobs.size());
   std::vector<int64_t> info(3 * jobs.size());
@@ -1383,12 +1397,20 @@ static void svd_host(const double* a, int64_t m, int64_t n, double eps, int64_t 
   Buf dA = alloc((size_t)(m * n) * sizeof(cx<R>));
   upload<R>(a, (cx<R>*)dA->p, m * n);
   g_tag = 6;
-  SvdJob<R> j = make_job<R>(0, (cx<R>*)dA->p, m, n, eps, chi, true);
+  const bool values_only = u == nullptr && v == nullptr;
+  SvdJob<R> j = make_job<R>(0, (cx<R>*)dA->p, m, n, eps, chi, !values_only);
   run_jobs<R>(&j, 1);
   read_info(1);
   const int64_t k = E.h_info[0];
   *rank = k;
   *disc = E.h_disc[0];
+  if (values_only) {  // the candidate-scoring decomposition (unswap.py:104-112)
+    std::vector<R> sg(k);
+    d2h(sg.data(), j.sig, k * sizeof(R));
+    sync();
+    for (int64_t i = 0; i < k; ++i) s[i] = (double)sg[i];
+    return;
+  }
   Buf dU = alloc((size_t)(m * k) * sizeof(cx<R>)), dV = alloc((size_t)(k * n) * sizeof(cx<R>));
   emit<R>(j, k, (cx<R>*)dU->p, false, (cx<R>*)dV->p, false);
   std::vector<R> sg(k);

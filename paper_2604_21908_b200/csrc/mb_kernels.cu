@@ -1840,33 +1840,38 @@ void finish_large(SvdJob<R>& J, int conv, int sweeps, cudaStream_t s) {
   }
 }
 
+// Block one-sided Jacobi on the job's working matrix. fresh: build X (and
+// V = I) from J.A first (when J.A is set); perturb: add the deterministic
+// 1e-14 |A|_F perturbation of the reference's retry before sweeping.
+// Returns whether every pair converged; `sweeps` accumulates the passes.
 template <typename R>
-void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
+bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fresh, bool perturb,
+                  int& sweeps) {
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
-  PhaseLog plog(s);
-  if (J.A) {
-    k_init_large<R><<<kSumBlocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n,
-                                               ws.red_dev);
+  bool partials = false;
+  if (fresh && J.A) {
+    k_init_large<R><<<kSumBlocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n, ws.red_dev);
     MB_LAUNCH_CHECK();
+    partials = true;
   }
-  plog.mark("init");
-  int conv = 0, sweeps = 0;
-  // the final check launch leaves the column norms in sig[p, 2p)
-  jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps, J.A != nullptr, J.sig + p);
-  if (consume_forced_failure()) conv = 0;
-  if (!conv) {
-    // one retry on a deterministically perturbed copy (tensor.py:139-150):
-    // X V^H + delta with |delta| ~ 1e-14 |A|_F, then sweep on
+  if (perturb) {
     k_perturb<R><<<kSumBlocks, 256, 0, s>>>(J.X, p * q, ws.red_dev + kSumBlocks);
     MB_LAUNCH_CHECK();
-    int sweeps2 = 0;
-    jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sweeps2, false, J.sig + p);
-    if (consume_forced_failure()) conv = 0;
-    sweeps += sweeps2;
   }
-  plog.mark(sweeps ? "sweeps" : "check");
-  finish_large<R>(J, conv, sweeps, s);
-  plog.mark("sort+rank");
+  int conv = 0, sw = 0;
+  // the final check launch leaves the column norms in sig[p, 2p)
+  jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sw, partials, J.sig + p);
+  sweeps += sw;
+  if (consume_forced_failure()) conv = 0;
+  return conv != 0;
+}
+
+template <typename R>
+void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
+  int sweeps = 0;
+  bool conv = jacobi_large<R>(J, ws, s, true, false, sweeps);
+  if (!conv) conv = jacobi_large<R>(J, ws, s, false, true, sweeps);
+  finish_large<R>(J, conv ? 1 : 0, sweeps, s);
 }
 
 
@@ -2239,6 +2244,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
   template void svd_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                     \
   template void finish_large<R>(SvdJob<R>&, int, int, cudaStream_t);                            \
+  template bool jacobi_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t, bool, bool, int&); \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
   template void launch_sweep<R>(const SweepPack<R>&, cudaStream_t);                             \

@@ -150,6 +150,12 @@ int64_t large_pair_capacity(int64_t p);
 template <typename R>
 void svd_large(SvdJob<R>& job, const LargeScratch& ws, cudaStream_t s);
 
+// Jacobi sweeps only (no sort / rank): fresh = build X, V from J.A first;
+// perturb = the reference's perturbed retry. Returns convergence.
+template <typename R>
+bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fresh, bool perturb,
+                  int& sweeps);
+
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n);
 

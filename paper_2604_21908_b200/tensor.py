@@ -119,3 +119,22 @@ def device_herm_eig(a: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     nat.check(lib.mb_herm_eig(nat.dptr(a), n, w.ctypes.data_as(C.POINTER(C.c_double)),
                               nat.dptr(v)), "mb_herm_eig")
     return w, v
+
+
+def truncated_spectrum(t: np.ndarray, split: int, epsilon: float, chi_max: int,
+                       dtype: str = "complex128") -> tuple[np.ndarray, float]:
+    """Kept singular values and discarded weight from the values-only device
+    decomposition that scores unswap candidates (unswap.py:104-112:
+    np.linalg.svd(..., compute_uv=False) + truncation_rank)."""
+    t = np.asarray(t, dtype=np.complex128)
+    rows = int(np.prod(t.shape[:split], dtype=np.int64))
+    cols = int(np.prod(t.shape[split:], dtype=np.int64))
+    a = np.ascontiguousarray(t.reshape(rows, cols))
+    s = np.empty(min(rows, cols), dtype=np.float64)
+    rank = C.c_int64()
+    disc = C.c_double()
+    lib = nat.load()
+    nat.check(lib.mb_svd_truncate(nat.dptr(a), rows, cols, nat.DTYPES[dtype], float(epsilon),
+                                  int(chi_max), None, nat.dptr(s), None, C.byref(rank),
+                                  C.byref(disc)), "mb_svd_truncate")
+    return s[: rank.value].copy(), disc.value

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import mirror_oracle as mo  # noqa: E402
 from paper_2604_21908_b200 import _native as nat  # noqa: E402
-from paper_2604_21908_b200.tensor import device_herm_eig, svd_truncate  # noqa: E402
+from paper_2604_21908_b200.tensor import device_herm_eig, svd_truncate, truncated_spectrum  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -127,16 +127,22 @@ def test_svd_truncate_gram_path(dtype):
         assert abs(res.discarded_weight - disc_ref) <= 10 * tol, name
         # U orthonormal, A_k reconstruction
         uu = res.u.conj().T @ res.u
-        assert np.max(np.abs(uu - np.eye(k))) <= (1e-9 if dtype == "complex128" else 1e-3), name
+        if dtype == "complex128":
+            assert np.max(np.abs(uu - np.eye(k))) <= 1e-9, name
+        else:  # fp32: columns far below sigma_max are orthogonal only to u32 sigma_max / sigma
+            big = res.s >= 1e-2 * res.s[0]
+            assert np.max(np.abs((uu - np.eye(k))[np.ix_(big, big)])) <= 1e-3, name
         ak = (res.u * res.s) @ res.v
         err = np.linalg.norm(a - ak)
         assert err <= np.sqrt(disc_ref) + (1e-10 if dtype == "complex128" else 1e-5), name
 
 
 def test_svd_retry_then_raise():
-    """tensor.py:139-150: one non-convergence is absorbed by a retry on a
-    perturbed copy (result within ~1e-14 |A|), a second one raises
-    SvdConvergenceError (large Jacobi path: p = 80 > 64, exact split)."""
+    """tensor.py:139-150 semantics on the large Jacobi path (p = 80 > 64,
+    exact split): a non-converged factorization is retried — first restarted
+    from the Gram eigenvectors, then on a deterministically perturbed copy
+    (result within ~1e-14 |A|) — and only a third failure raises
+    SvdConvergenceError."""
     from paper_2604_21908_b200.tensor import SvdConvergenceError
 
     lib = nat.load()
@@ -148,6 +154,10 @@ def test_svd_retry_then_raise():
         recon = (dec.u * dec.s) @ dec.v
         assert np.abs(recon - a).max() <= 1e-10 * np.abs(a).max()
         lib.mb_debug_fail_svd(2)
+        dec = svd_truncate(a, 1, 0.0, 1000)
+        recon = (dec.u * dec.s) @ dec.v
+        assert np.abs(recon - a).max() <= 1e-10 * np.abs(a).max()
+        lib.mb_debug_fail_svd(3)
         with pytest.raises(SvdConvergenceError):
             svd_truncate(a, 1, 0.0, 1000)
     finally:
@@ -171,3 +181,23 @@ def test_flat_blob_from_c36():
         assert np.all(np.isfinite(res.u)) and np.all(np.isfinite(res.v))
         ak = (res.u * res.s) @ res.v
         assert np.linalg.norm(a - ak) <= (1e-12 if dtype == "complex128" else 1e-5)
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_values_only_spectrum(dtype):
+    """Candidate scoring (unswap.py:104-112): the values-only decomposition
+    (Gram tridiagonalization + bisection for p >= 512) keeps LAPACK's rank."""
+    rng = np.random.default_rng(21)
+    eps = 2e-3
+    for name, a in [("lowrank", _crandn(rng, 768, 160) @ _crandn(rng, 160, 640)),
+                    ("flat", 0.1 * (_unitary(rng, 600)[:, :300] @ _unitary(rng, 600)[:, :300].conj().T)),
+                    ("graded", (_unitary(rng, 700) * np.logspace(0, -5, 700)) @ _unitary(rng, 700).conj().T)]:
+        a = a / np.linalg.norm(a)
+        if dtype == "complex64":
+            a = a.astype(np.complex64).astype(np.complex128)
+        sref = np.linalg.svd(a, compute_uv=False)
+        s, disc = truncated_spectrum(a, 1, eps, 8192, dtype=dtype)
+        if dtype == "complex128":
+            assert len(s) == mo.kept_rank(sref, eps, 8192), name
+        tol = 1e-12 if dtype == "complex128" else 2e-5
+        assert np.max(np.abs(s - sref[:len(s)])) <= max(tol, 1e-7 if dtype == "complex128" else 0) * sref[0] * 10, name
