@@ -214,7 +214,8 @@ constexpr int TBM = 64, TBN = 64;
 
 template <typename TI, typename TC, bool CA, bool CB, int BK>
 __global__ void __launch_bounds__(256) k_gemm_cm(const GemmDesc* __restrict__ descs, GemmDesc one,
-                                                 double alpha, double beta, int64_t kslice) {
+                                                 double alpha, double beta, int64_t kslice,
+                                                 int lower = 0) {
   __shared__ TC As[BK][TBM + 1];
   __shared__ TC Bs[BK][TBN + 1];
   GemmDesc d = descs ? descs[blockIdx.z] : one;
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(256) k_gemm_cm(const GemmDesc* __restrict__ de
   const int64_t M = d.M, N = d.N, K = d.K;
   const int64_t m0 = (int64_t)blockIdx.x * TBM, n0 = (int64_t)blockIdx.y * TBN;
   if (m0 >= M || n0 >= N) return;
+  if (lower && m0 + TBM <= n0) return;  // tile strictly above the diagonal
   const TI* A = (const TI*)d.A;
   const TI* B = (const TI*)d.B;
   TC* C = (TC*)d.C;
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(256) k_gemm_cm(const GemmDesc* __restrict__ de
 template <typename TI, typename TC, bool CA, bool CB>
 static void gemm_cm(int stage, int64_t M, int64_t N, int64_t K, double alpha, const TI* A,
                     int64_t lda, const TI* B, int64_t ldb, double beta, TC* C, int64_t ldc,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool lower = false) {
   if (M <= 0 || N <= 0) return;
   // algorithmic traffic: read A and B once, write C (read C too when beta != 0)
   const double by = (double)sizeof(TI) * (double)(M * K + K * N) +
@@ -307,7 +309,7 @@ static void gemm_cm(int stage, int64_t M, int64_t N, int64_t K, double alpha, co
   GemmDesc d{M, N, K, A, lda, B, ldb, C, ldc};
   constexpr int BK = sizeof(TC) >= 16 ? 8 : 16;
   dim3 grid((unsigned)ediv(M, TBM), (unsigned)ediv(N, TBN), 1);
-  k_gemm_cm<TI, TC, CA, CB, BK><<<grid, 256, 0, s>>>(nullptr, d, alpha, beta, 0);
+  k_gemm_cm<TI, TC, CA, CB, BK><<<grid, 256, 0, s>>>(nullptr, d, alpha, beta, 0, lower ? 1 : 0);
   EIG_CHECK();
 }
 
@@ -627,6 +629,7 @@ __global__ void __launch_bounds__(256) k_trd_symv(const zd* __restrict__ A, int6
 // W^H v), k_trd_symv2 (y = A22 v - W p1 - V p2, partial y^H v). All partial
 // sums are reduced in a fixed order (bitwise reproducible).
 constexpr int kRowBlk = 256;    // rows per block in upd / vec
+constexpr int64_t kGridRows = 768;  // trailing size above which the grid path runs
 constexpr int kMaxSymvBlk = 1184;
 constexpr int kPartStride = 4 * kNB + 4;  // doubles per block partial
 
@@ -842,12 +845,135 @@ __global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, in
   }
 }
 
+// Hermitian matrix-vector product from the lower triangle only (half the
+// HBM traffic of a full-column sweep): the trailing block [s, n)^2 is tiled
+// 64 x 64; a lower tile (I, J), I > J, contributes A_IJ v_J to y_I and
+// A_IJ^H v_I to y_J, a diagonal tile its Hermitian completion to y_I. Each
+// contribution lands in its own slot P[row tile][other tile] (no atomics);
+// k_symv_sum adds the slots in a fixed order.
+constexpr int kST = 64;
+
+__global__ void __launch_bounds__(256) k_symv_tiles(const zd* __restrict__ A, int64_t n, int64_t s0,
+                                                    const zd* __restrict__ v, int nt,
+                                                    zd* __restrict__ P) {
+  __shared__ zd vI[kST], vJ[kST];
+  __shared__ zd rowp[4][kST];
+  __shared__ zd colp[2][4][16];
+  // lower-tile index -> (I, J), I >= J
+  const int64_t t = blockIdx.x;
+  int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= t) ++I;
+  while ((int64_t)I * (I + 1) / 2 > t) --I;
+  const int J = (int)(t - (int64_t)I * (I + 1) / 2);
+  const int tid = threadIdx.x, tr = tid & 63, tg = tid >> 6;
+  const int64_t r0 = s0 + (int64_t)I * kST, c0 = s0 + (int64_t)J * kST;
+  if (tid < kST) {
+    vI[tid] = r0 + tid < n ? v[r0 + tid] : mk<double>(0, 0);
+    vJ[tid] = c0 + tid < n ? v[c0 + tid] : mk<double>(0, 0);
+  }
+  __syncthreads();
+  const int64_t r = r0 + tr;
+  zd a[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int cc = tg * 16 + u;
+    const int64_t c = c0 + cc;
+    a[u] = (r < n && c < n && (I != J || tr >= cc)) ? A[r + c * n] : mk<double>(0, 0);
+  }
+  zd acc = mk<double>(0, 0);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc = cadd(acc, cmul(a[u], vJ[tg * 16 + u]));
+  rowp[tg][tr] = acc;
+  // column part: conj(A_rc) v_r summed over the tile's rows (strictly lower)
+  const int lane = tid & 31, half = (tid >> 5) & 1;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int cc = tg * 16 + u;
+    zd x = (I != J || tr > cc) ? cmulc(a[u], vI[tr]) : mk<double>(0, 0);
+    x.x = warp_sum(x.x);
+    x.y = warp_sum(x.y);
+    if (lane == 0) colp[half][tg][u] = x;
+  }
+  __syncthreads();
+  zd* PI = P + ((int64_t)I * nt + J) * kST;  // slot of (I, J) in row tile I
+  zd* PJ = P + ((int64_t)J * nt + I) * kST;  // slot of (I, J) in row tile J
+  if (tid < kST) {
+    zd y = cadd(cadd(rowp[0][tid], rowp[1][tid]), cadd(rowp[2][tid], rowp[3][tid]));
+    if (I == J) {
+      // diagonal tile: the strictly-lower part's transpose contribution
+      const zd cpart = cadd(colp[0][tid >> 4][tid & 15], colp[1][tid >> 4][tid & 15]);
+      y = cadd(y, cpart);
+    }
+    PI[tid] = y;
+  } else if (tid < 2 * kST && I != J) {
+    const int cc = tid - kST;
+    PJ[cc] = cadd(colp[0][cc >> 4][cc & 15], colp[1][cc >> 4][cc & 15]);
+  }
+}
+
+// y[r] = sum_slot P[r tile][slot][r] - sum_{t<i} (W[r,t] p1[t] + V[r,t] p2[t]),
+// plus the per-block partial y^H v (as k_trd_symv2)
+__global__ void __launch_bounds__(256) k_symv_sum(const zd* __restrict__ P, int nt, int64_t n,
+                                                  int64_t s0, const zd* __restrict__ VW, int i,
+                                                  const double* __restrict__ part_p, int nblk_p,
+                                                  zd* __restrict__ y, double* __restrict__ part_yv) {
+  __shared__ zd pv[2 * kNB];
+  __shared__ double red[32];
+  const zd* V = VW;
+  const zd* W = VW + (int64_t)kNB * n;
+  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
+    const int t = e < i ? e : kNB + (e - i);
+    double re = 0, im = 0;
+    for (int bb = 0; bb < nblk_p; ++bb) {
+      re += part_p[(int64_t)bb * kPartStride + 2 * t];
+      im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
+    }
+    pv[t] = mk<double>(re, im);
+  }
+  __syncthreads();
+  const int64_t r = s0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const zd* v = V + (int64_t)i * n;
+  double yr = 0, yi = 0;
+  if (r < n) {
+    const int64_t rr = r - s0;
+    const int64_t I = rr / kST, off = rr % kST;
+    zd acc = mk<double>(0, 0);
+    const zd* Pr = P + I * nt * kST + off;
+    for (int sl = 0; sl < nt; ++sl) acc = cadd(acc, Pr[(int64_t)sl * kST]);
+    for (int t = 0; t < i; ++t) {
+      acc = csub(acc, cmul(W[r + t * n], pv[t]));
+      acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
+    }
+    y[r] = acc;
+    const zd yv = cmulc(acc, v[r]);
+    yr = yv.x;
+    yi = yv.y;
+  }
+  yr = block_sum(yr, red);
+  __syncthreads();
+  yi = block_sum(yi, red);
+  if (threadIdx.x == 0) {
+    part_yv[(int64_t)blockIdx.x * kPartStride] = yr;
+    part_yv[(int64_t)blockIdx.x * kPartStride + 1] = yi;
+  }
+}
+
+// Hermitian completion of the trailing block [s, n)^2 from its lower triangle
+__global__ void k_symmetrize(zd* __restrict__ A, int64_t n, int64_t s0) {
+  const int64_t m = n - s0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = s0 + e % m, c = s0 + e / m;
+    if (r < c) A[r + c * n] = cconj(A[c + r * n]);
+  }
+}
+
 __global__ void k_trd_last(const zd* __restrict__ A, int64_t n, double* __restrict__ dd) {
   dd[n - 1] = A[(n - 1) + (n - 1) * n].x;
 }
 
 static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* pv, zd* y,
-                  double* part, cudaStream_t s) {
+                  double* part, zd* slots, cudaStream_t s) {
   if (n == 1) {
     k_trd_last<<<1, 1, 0, s>>>(A, n, d);
     EIG_CHECK();
@@ -859,11 +985,18 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
   double* part_yv = part + 2 * (size_t)kMaxSymvBlk * kPartStride;
   const int64_t nref = n - 1;
   int nblk_yv = 0;  // blocks of the previous column's symv (grid path)
+  bool upper_stale = false;  // the grid path keeps only the lower triangle current
   for (int64_t j0 = 0; j0 < nref; j0 += kNB) {
     const int b = (int)std::min<int64_t>(kNB, nref - j0);
     // one CTA per panel step while the trailing block is small; the grid
     // path above ~768 rows
-    const bool grid = n - j0 > 768;
+    const bool grid = n - j0 > kGridRows;
+    if (!grid && upper_stale) {
+      const int64_t m = n - j0;
+      k_symmetrize<<<(int)std::min<int64_t>(ediv(m * m, 256), 148 * 8), 256, 0, s>>>(A, n, j0);
+      EIG_CHECK();
+      upper_stale = false;
+    }
     for (int i = 0; i <= b; ++i) {
       const int64_t c = j0 + i;
       const double rows = (double)(n - c);
@@ -897,10 +1030,15 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
         EIG_CHECK();
       }
       {
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ediv(rw, 8), kMaxSymvBlk));
-        EigScope sc(ES_TRD_SYMV, s, 16.0 * (double)rw * (double)rw + 16.0 * rw * (2.0 * i + 2.0),
+        // lower triangle of the trailing block read once: rw (rw + 1) / 2 complex
+        const int nt = (int)ediv(rw, kST);
+        const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
+        EigScope sc(ES_TRD_SYMV, s, 8.0 * (double)rw * (double)(rw + 1) + 16.0 * rw * (2.0 * i + 2.0),
                     8.0 * (double)rw * (double)rw);
-        k_trd_symv2<<<blocks, 256, 0, s>>>(A, n, VW, c, i, part_p, nblk_v, y, part_yv);
+        k_symv_tiles<<<(unsigned)ntiles, 256, 0, s>>>(A, n, c + 1, VW + (int64_t)i * n, nt, slots);
+        EIG_CHECK();
+        const int blocks = (int)ediv(rw, 256);
+        k_symv_sum<<<blocks, 256, 0, s>>>(slots, nt, n, c + 1, VW, i, part_p, nblk_v, y, part_yv);
         EIG_CHECK();
         nblk_yv = blocks;
       }
@@ -912,6 +1050,9 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
       const zd* V2 = VW + t0;
       const zd* W2 = VW + (int64_t)kNB * n + t0;
       zd* C = A + t0 + t0 * n;
+      // the next panel on the grid path reads only the lower triangle
+      const bool lower = n - t0 > kGridRows;
+      upper_stale = upper_stale || lower;
       if (b == kNB) {
         {
           EigScope sc(ES_TRD_UPDATE, s, 32.0 * (double)(m * b), 0.0);
@@ -919,10 +1060,11 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
               VW + t0, VW + 2 * (int64_t)kNB * n + t0, m, b, n);
           EIG_CHECK();
         }
-        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, 2 * b, -1.0, V2, n, W2, n, 1.0, C, n, s);
+        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, 2 * b, -1.0, V2, n, W2, n, 1.0, C, n, s,
+                                     lower);
       } else {
-        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, V2, n, W2, n, 1.0, C, n, s);
-        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, W2, n, V2, n, 1.0, C, n, s);
+        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, V2, n, W2, n, 1.0, C, n, s, lower);
+        gemm_cm<zd, zd, false, true>(ES_TRD_UPDATE, m, m, b, -1.0, W2, n, V2, n, 1.0, C, n, s, lower);
       }
     }
   }
@@ -1390,7 +1532,7 @@ struct EigLayout {
 enum {
   L_G, L_VC, L_QA, L_QS, L_SV, L_VW, L_D, L_E, L_TAU, L_PV, L_Y, L_DS, L_ZS, L_PERM, L_ACT, L_RCS,
   L_SLOT, L_END, L_K, L_DND, L_ZND, L_ORG, L_TAUS, L_ZH, L_RHO, L_MG, L_LEAF, L_GD, L_FAIL, L_YB,
-  L_T, L_W1, L_W2, L_YTY, L_PART, L_SPLIT, L_NUM
+  L_T, L_W1, L_W2, L_YTY, L_PART, L_SPLIT, L_SYMV, L_NUM
 };
 
 static void layout(int64_t n, size_t* off, size_t& total) {
@@ -1425,6 +1567,7 @@ static void layout(int64_t n, size_t* off, size_t& total) {
       (size_t)kNBT * kNBT * 16 * kMaxSplit,         // YtY (+ split-K partials of YtY)
       3 * (size_t)kMaxSymvBlk * kPartStride * 8,    // hetrd partial sums
       (size_t)n * kNBT * 16 * kMaxSplit,            // split-K partials (back-transform)
+      (size_t)ediv(n, 64) * ediv(n, 64) * 64 * 16,  // lower-triangle matvec slots
   };
   size_t o = 0;
   for (int i = 0; i < L_NUM; ++i) {
@@ -1563,7 +1706,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
 
   // 2. tridiagonalize
   dbg_check("gram", G, 2 * n * n, s);
-  hetrd(G, n, VW, d, e, tau, pv, y, (double*)(B + off[L_PART]), s);
+  hetrd(G, n, VW, d, e, tau, pv, y, (double*)(B + off[L_PART]), (zd*)(B + off[L_SYMV]), s);
   dbg_check("d", d, n, s);
   dbg_check("e", e, n - 1, s);
 
@@ -1874,7 +2017,7 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
     double* w = (double*)(B + off[L_DS]);
     dbg_check("gram", G, 2 * p * p, s);
     hetrd(G, p, VW, d, e, (zd*)(B + off[L_TAU]), (zd*)(B + off[L_PV]), (zd*)(B + off[L_Y]),
-          (double*)(B + off[L_PART]), s);
+          (double*)(B + off[L_PART]), (zd*)(B + off[L_SYMV]), s);
     {
       EigScope sc(ES_DC, s, 16.0 * (double)p, 0.0);
       k_bisect<<<(int)ediv(p, 256), 256, 0, s>>>(d, e, p, w);
