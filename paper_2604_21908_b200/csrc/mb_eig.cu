@@ -1539,7 +1539,7 @@ static void layout(int64_t n, size_t* off, size_t& total) {
   const size_t nn = (size_t)n * (size_t)n;
   const size_t sz[L_NUM] = {
       nn * 16,                       // G
-      nn * 16,                       // Vc
+      0,                             // Vc (aliases Qs + Sv, free after divide and conquer)
       nn * 8,                        // Qa
       nn * 8,                        // Qs
       nn * 8,                        // Sv
@@ -1674,7 +1674,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
   layout(n, off, total);
   char* B = base_ptr(ws);
   zd* G = (zd*)(B + off[L_G]);
-  zd* Vc = (zd*)(B + off[L_VC]);
+  zd* Vc = (zd*)(B + off[L_QS]);
   double* Qa = (double*)(B + off[L_QA]);
   double* Qs = (double*)(B + off[L_QS]);
   double* Sv = (double*)(B + off[L_SV]);
@@ -1975,7 +1975,7 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
   layout(p, off, total);
   char* B = base_ptr(ws);
   zd* G = (zd*)(B + off[L_G]);
-  zd* Vc = (zd*)(B + off[L_VC]);
+  zd* Vc = (zd*)(B + off[L_QS]);
   if (J.A) {
     const int blocks = (int)std::min<int64_t>(ediv(p * q, 256), 148 * 16);
     k_gram_init_x<R><<<blocks, 256, 0, s>>>(J.A, J.X, m, n);
@@ -2060,7 +2060,7 @@ void gram_precondition(SvdJob<R>& J, void* ws, cudaStream_t s) {
   layout(p, off, total);
   char* B = base_ptr(ws);
   zd* G = (zd*)(B + off[L_G]);
-  zd* Vc = (zd*)(B + off[L_VC]);
+  zd* Vc = (zd*)(B + off[L_QS]);
   gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s);
   heevd(p, ws, s, nullptr);
   cx<R>* VG = reinterpret_cast<cx<R>*>(J.W + q * p);
@@ -2124,7 +2124,7 @@ int herm_eig_device(const zd* G_in, int64_t n, double* w_out, zd* V_out, void* w
   k_sort_eig<<<(int)ediv(n, 256), 256, 0, s>>>(d, n, perm);
   EIG_CHECK();
   k_apply_eig_perm<<<(int)std::min<int64_t>(ediv(n * n, 256), 148 * 16), 256, 0, s>>>(
-      perm, d, (const zd*)(B + off[L_VC]), n, w_out, V_out);
+      perm, d, (const zd*)(B + off[L_QS]), n, w_out, V_out);
   EIG_CHECK();
   cudaStreamSynchronize(s);
   const int f = *fail_h;

@@ -111,7 +111,23 @@ static Buf alloc(size_t bytes) {
   auto b = std::make_shared<DevBuf>();
   b->bytes = bytes;
   b->s = E.stream;
-  if (bytes) ck(cudaMallocAsync(&b->p, bytes, E.stream), "cudaMallocAsync");
+  if (bytes) {
+    cudaError_t e = cudaMallocAsync(&b->p, bytes, E.stream);
+    if (e == cudaErrorMemoryAllocation) {
+      // the stream-ordered pool keeps freed blocks (release threshold = max);
+      // blocks outgrown by the grow-only scratch fragment it. Drain, hand the
+      // unused reserve back, retry once.
+      cudaGetLastError();
+      ck(cudaDeviceSynchronize(), "sync before pool trim");
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      ck(cudaDeviceGetDefaultMemPool(&pool, dev), "default mempool");
+      ck(cudaMemPoolTrimTo(pool, 0), "mempool trim");
+      e = cudaMallocAsync(&b->p, bytes, E.stream);
+    }
+    ck(e, "cudaMallocAsync");
+  }
   return b;
 }
 
@@ -1899,7 +1915,20 @@ int mb_trial_pair(const mb_chain* c, int nl, const int* kinds_l, const int* qubi
     require(out_l && out_r, "null output handle");
     std::unique_ptr<mb_chain> l(new mb_chain(*c));
     std::unique_ptr<mb_chain> r(new mb_chain(*c));
-    if (c->dtype == MB_C64)
+    // chains with bonds >= 1024 (blobs >= 4096 wide) saturate the GPU with
+    // one trial and would double the large-SVD workspaces: run the two
+    // trials one after the other on the main context (same results)
+    int64_t maxb = 1;
+    for (auto& st : c->s) maxb = std::max(maxb, std::max(st.l, st.r));
+    if (maxb >= 1024) {
+      if (c->dtype == MB_C64) {
+        trial<float>(*l, nl, kinds_l, qubits_l, mats_l, MB_SIDE_LEFT, eps, chi);
+        trial<float>(*r, nr, kinds_r, qubits_r, mats_r, MB_SIDE_RIGHT, eps, chi);
+      } else {
+        trial<double>(*l, nl, kinds_l, qubits_l, mats_l, MB_SIDE_LEFT, eps, chi);
+        trial<double>(*r, nr, kinds_r, qubits_r, mats_r, MB_SIDE_RIGHT, eps, chi);
+      }
+    } else if (c->dtype == MB_C64)
       trial_pair<float>(*l, nl, kinds_l, qubits_l, mats_l, *r, nr, kinds_r, qubits_r, mats_r, eps, chi);
     else
       trial_pair<double>(*l, nl, kinds_l, qubits_l, mats_l, *r, nr, kinds_r, qubits_r, mats_r, eps, chi);

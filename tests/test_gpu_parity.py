@@ -427,17 +427,21 @@ def test_concurrent_trials_match_sequential(golden, name):
     np.testing.assert_array_equal(dense_output(seq), dense_output(par))
 
 
-def test_c36_prefix_trace_matches_oracle():
-    """Large-scale parity: the first 160 absorption steps of the bench's 36q
-    instance (7 unswap calls, MPO up to 7M elements, bonds up to 1024) take
-    exactly the oracle's decisions (tests/golden/make_c36_prefix.py)."""
+@pytest.mark.parametrize("fixture", ["c36_prefix160_trace.json", "c36_prefix767_trace.json"])
+def test_c36_prefix_trace_matches_oracle(fixture):
+    """Large-scale parity on configs[2]: the first 160 / 767 absorption steps
+    of the bench's 36q instance (up to 43 unswap calls, MPO up to 7M
+    elements, bonds up to 1024, large truncated splits through the Gram
+    eigensolver) take exactly the oracle's decisions: identical trace records
+    (phase, unitaries consumed, elements). Fixtures streamed from the oracle
+    (tests/golden/make_c36_prefix.py, make_long_trace.py)."""
     import json
     from pathlib import Path
 
     from bench import _instance
     from paper_2604_21908_b200 import Contraction
 
-    ref = json.loads((Path(__file__).resolve().parent / "golden" / "c36_prefix160_trace.json").read_text())
+    ref = json.loads((Path(__file__).resolve().parent / "golden" / fixture).read_text())
     job = Contraction(_instance("c36").circuit, ContractionConfig())
     job.advance(max_steps=ref["steps"])
     got = [[t.phase, t.unitaries_consumed, t.elements] for t in job.trace]

@@ -32,8 +32,14 @@ def main():
     ap.add_argument("--chunk", type=int, default=8)
     ap.add_argument("--serial", action="store_true", help="sequential adaptive trials")
     ap.add_argument("--trace-out", default=None, help="write the trace records (JSON lines)")
+    ap.add_argument("--seed", type=int, default=None, help="instance seed override")
     a = ap.parse_args()
-    inst = _instance(a.config)
+    if a.seed is not None:
+        from paper_2604_21908_b200.peaked import generate
+        n, depth, w, obf, _, hidden = CONFIGS[a.config]
+        inst = generate(n, depth, w, obf, a.seed, hidden_permutation=hidden)
+    else:
+        inst = _instance(a.config)
     nat.load()
     c0 = nat.counters()
     l0 = nat.launch_count()
