@@ -1627,7 +1627,9 @@ __global__ void k_real_to_cx(const double* __restrict__ Z, zd* __restrict__ V, i
 }
 
 static void backtransform(const zd* A, const zd* tau, int64_t n, zd* V, zd* Ybuf, zd* T, zd* W1,
-                          zd* W2, zd* YtY, zd* part, cudaStream_t s) {
+                          zd* W2, zd* YtY, zd* part, cudaStream_t s, int64_t ncols = -1) {
+  // V is n x ncols (column-major, ld n): only those columns are transformed
+  if (ncols < 0) ncols = n;
   const int64_t nref = n - 1;
   if (nref <= 0) return;
   static bool attr = (cudaFuncSetAttribute(k_bt_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1654,10 +1656,10 @@ static void backtransform(const zd* A, const zd* tau, int64_t n, zd* V, zd* Ybuf
       EIG_CHECK();
     }
     zd* Vs = V + (b0 + 1);
-    gemm_cm_splitk<zd, zd, true, false>(ES_BT, b, n, L, 1.0, Ybuf, L, Vs, n, 0.0, W1, kNBT, part,
+    gemm_cm_splitk<zd, zd, true, false>(ES_BT, b, ncols, L, 1.0, Ybuf, L, Vs, n, 0.0, W1, kNBT, part,
                                         part_cap, s);
-    gemm_cm<zd, zd, false, false>(ES_BT, b, n, b, 1.0, T, kNBT, W1, kNBT, 0.0, W2, kNBT, s);
-    gemm_cm<zd, zd, false, false>(ES_BT, L, n, b, -1.0, Ybuf, L, W2, kNBT, 1.0, Vs, n, s);
+    gemm_cm<zd, zd, false, false>(ES_BT, b, ncols, b, 1.0, T, kNBT, W1, kNBT, 0.0, W2, kNBT, s);
+    gemm_cm<zd, zd, false, false>(ES_BT, L, ncols, b, -1.0, Ybuf, L, W2, kNBT, 1.0, Vs, n, s);
   }
 }
 
@@ -1669,7 +1671,7 @@ static char* base_ptr(void* ws) { return reinterpret_cast<char*>(ws); }
 // eigenvalues into w (device, n doubles, unordered), eigenvectors as the
 // columns of Vc (n x n complex column-major). Returns the number of leaf QL
 // iterations that failed to converge (0 = success) — read back synchronously.
-static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
+static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host, bool back = true) {
   size_t off[L_NUM], total;
   layout(n, off, total);
   char* B = base_ptr(ws);
@@ -1794,6 +1796,7 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
     }
   }
   }
+  if (!back) return;  // caller back-transforms a subset of the columns
   // 4. V = Q_H Z
   {
     const int64_t nn = n * n;
@@ -1806,6 +1809,66 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host) {
   if (fail_host) {
     cudaMemcpyAsync(fail_host, fail, sizeof(int), cudaMemcpyDeviceToHost, s);
   }
+}
+
+
+// descending order of the eigenvalues (rank by count, ties by index)
+__global__ void k_order_desc(const double* __restrict__ w, int64_t n, int* __restrict__ order,
+                             double* __restrict__ wsorted) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const double v = w[c];
+    int64_t pos = 0;
+    for (int64_t t = 0; t < n; ++t) pos += (w[t] > v) || (w[t] == v && t < c);
+    order[pos] = (int)c;
+    wsorted[pos] = v;
+  }
+}
+
+// Vc[:, t] = (Z[:, order[t]], 0) for t < k
+__global__ void k_gather_cols(const double* __restrict__ Z, const int* __restrict__ order,
+                              int64_t n, int64_t k, zd* __restrict__ Vc) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % n, t = e / n;
+    Vc[e] = mk<double>(Z[r + (int64_t)order[t] * n], 0.0);
+  }
+}
+
+// sig for the columns past the kept subspace: sqrt(max(lambda, 0))
+template <typename R>
+__global__ void k_sig_tail(const double* __restrict__ wsorted, int64_t k, int64_t p,
+                           R* __restrict__ sig) {
+  for (int64_t c = k + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < p;
+       c += (int64_t)gridDim.x * blockDim.x)
+    sig[c] = (R)sqrt(fmax(wsorted[c], 0.0));
+}
+
+// Host: how many leading eigenvectors the truncated factorization can need.
+// The reference rule (tensor.py:119-136) on sigma_lambda = sqrt(lambda),
+// then generously widened: every value within half the boundary value (the
+// column-norm sigma differ from sigma_lambda far less), ties, +32.
+static int64_t keep_columns(const std::vector<double>& wdesc, double eps, int64_t chi) {
+  const int64_t p = (int64_t)wdesc.size();
+  std::vector<double> sg(p);
+  double total = 0;
+  for (int64_t i = 0; i < p; ++i) {
+    sg[i] = std::sqrt(std::max(wdesc[i], 0.0));
+    total += sg[i] * sg[i];
+  }
+  const double budget = eps * eps * total;
+  int64_t r = p;
+  double tail = 0;
+  for (int64_t k = p; k >= 1; --k) {
+    if (tail <= budget) r = k;
+    else break;
+    tail += sg[k - 1] * sg[k - 1];
+  }
+  r = std::min<int64_t>(r, chi);
+  const double edge = sg[std::max<int64_t>(r, 1) - 1];
+  int64_t k = r;
+  while (k < p && sg[k] >= 0.5 * edge) ++k;
+  return std::min<int64_t>(p, k + 32);
 }
 
 // ---- values only: bisection on the tridiagonal ---------------------------------
@@ -2027,24 +2090,50 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
     }
     return;
   }
-  // 2-4. eigenvectors of G
-  heevd(p, ws, s, nullptr);
-  // 5. V in the job precision, Y = X V, sigma = column norms of Y
-  cx<R>* V = J.V ? J.V : reinterpret_cast<cx<R>*>(J.W + q * p);
+  // 2-3. tridiagonalize + divide and conquer (eigenvalues, eigenvectors of T)
+  heevd(p, ws, s, nullptr, false);
+  // only the leading eigenvectors the truncation can keep are
+  // back-transformed and multiplied by X (one read-back of the spectrum)
+  double* wsorted = (double*)(B + off[L_DS]);
+  int* order = (int*)(B + off[L_PERM]);
   {
-    const int blocks = (int)std::min<int64_t>(ediv(p * p, 256), 148 * 16);
-    k_cvt_v<R><<<blocks, 256, 0, s>>>(Vc, V, p * p);
+    EigScope sc(ES_DC, s, 8.0 * (double)p, 0.0);
+    k_order_desc<<<(int)ediv(p, 256), 256, 0, s>>>((double*)(B + off[L_D]), p, order, wsorted);
     EIG_CHECK();
   }
-  dbg_check("Vc", Vc, 2 * p * p, s);
+  std::vector<double> wd((size_t)p);
+  cudaMemcpyAsync(wd.data(), wsorted, sizeof(double) * (size_t)p, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  const int64_t kc = keep_columns(wd, J.eps, J.chi);
+  {
+    EigScope sc(ES_BT, s, 24.0 * (double)(p * kc), 0.0);
+    k_gather_cols<<<(int)std::min<int64_t>(ediv(p * kc, 256), 148 * 16), 256, 0, s>>>(
+        (const double*)(B + off[L_QA]), order, p, kc, Vc);
+    EIG_CHECK();
+  }
+  backtransform(G, (const zd*)(B + off[L_TAU]), p, Vc, (zd*)(B + off[L_YB]), (zd*)(B + off[L_T]),
+                (zd*)(B + off[L_W1]), (zd*)(B + off[L_W2]), (zd*)(B + off[L_YTY]),
+                (zd*)(B + off[L_SPLIT]), s, kc);
+  // 5. V (kept columns) in the job precision, Y = X V, sigma = column norms
+  cx<R>* V = J.V;
+  {
+    const int blocks = (int)std::min<int64_t>(ediv(p * kc, 256), 148 * 16);
+    k_cvt_v<R><<<blocks, 256, 0, s>>>(Vc, V, p * kc);
+    EIG_CHECK();
+  }
   cx<R>* Y = J.W;
-  gemm_cm<cx<R>, cx<R>, false, false>(ES_XV, q, p, p, 1.0, J.X, q, V, p, 0.0, Y, q, s);
+  gemm_cm<cx<R>, cx<R>, false, false>(ES_XV, q, kc, p, 1.0, J.X, q, V, p, 0.0, Y, q, s);
   J.X = Y;
   {
-    EigScope sc(ES_XV, s, (double)sizeof(cx<R>) * (double)(q * p), 4.0 * (double)(q * p));
-    const int blocks = (int)std::min<int64_t>(ediv(p * 32, 256), 148 * 8);
-    k_colnorms<R><<<blocks, 256, 0, s>>>(Y, q, p, J.sig + p);
+    EigScope sc(ES_XV, s, (double)sizeof(cx<R>) * (double)(q * kc), 4.0 * (double)(q * kc));
+    const int blocks = (int)std::min<int64_t>(ediv(kc * 32, 256), 148 * 8);
+    k_colnorms<R><<<blocks, 256, 0, s>>>(Y, q, kc, J.sig + p);
     EIG_CHECK();
+    if (kc < p) {
+      k_sig_tail<R><<<(int)std::min<int64_t>(ediv(p - kc, 256), 148), 256, 0, s>>>(wsorted, kc, p,
+                                                                                  J.sig + p);
+      EIG_CHECK();
+    }
   }
 }
 
