@@ -61,22 +61,30 @@ def _args():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c56")
     ap.add_argument("--warm-prefix", type=int, default=64,
                     help="absorption steps per warm-up step on c36/c56 (0 = full contractions)")
+    ap.add_argument("--prefix-steps", type=int, default=None,
+                    help="absorption steps per timed step (default: 400 on c56/c36, i.e. a fixed "
+                         "prefix of the contraction; 0 = the full contraction to the peak)")
     ap.add_argument("--dtype", choices=["complex128", "complex64"], default="complex128")
+    ap.add_argument("--seed", type=int, default=None, help="instance seed override")
     ap.add_argument("--cpu-sample-s", type=float, default=20.0,
                     help="CPU work per reference-arm sample (seconds, approx.)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
+_SEED = {}
+
+
 def _instance(name):
     from paper_2604_21908_b200.peaked import generate
 
     n, depth, w, obf, seed, hidden = CONFIGS[name]
-    return generate(n, depth, w, obf, seed, hidden_permutation=hidden)
+    return generate(n, depth, w, obf, _SEED.get(name, seed), hidden_permutation=hidden)
 
 
 def _workload(name, dtype):
     n, depth, w, obf, seed, hidden = CONFIGS[name]
+    seed = _SEED.get(name, seed)
     return {"workload": f"{n}q peaked circuit, middle-MPO contraction + peak extraction",
             "config": name, "qubits": n, "depth_budget": depth, "obfuscation_swaps": obf,
             "seed": seed, "epsilon": 2e-3, "chi_max": 8192, "tau": 1_000_000,
@@ -336,6 +344,8 @@ def _phase_seconds(trace):
 
 def main():
     args = _args()
+    if args.seed is not None:
+        _SEED[args.config] = args.seed
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -377,8 +387,13 @@ def main():
     n2q = inst.circuit.two_qubit_count()
     big = args.config in ("c36", "c56")
 
+    prefix = args.prefix_steps if args.prefix_steps is not None else (400 if big else 0)
+
     def one_step():
         job = Contraction(inst.circuit, cfg, comm)
+        if prefix:
+            job.advance(max_steps=prefix)
+            return job, None
         job.advance()
         res = job.finish()
         return job, peak_output(res)
@@ -429,7 +444,10 @@ def main():
     if dist:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     dev_ms = float(t_max.item())
-    total_gates = n2q * args.steps  # one (replicated) contraction per step
+    # source two-qubit gates absorbed per step (all of them for a full
+    # contraction; the prefix's own count otherwise)
+    gates_step = [j.consumed_source for j in jobs]
+    total_gates = sum(gates_step)
     value = total_gates / (dev_ms / 1e3)
 
     # ---- e2e: through the public API from QASM text to the host bitstring ----
@@ -438,11 +456,17 @@ def main():
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    bits = None
     for _ in range(args.steps):
         circ = parse_qasm(qasm)
         job = Contraction(circ, cfg, comm)
-        job.advance()
-        bits, p = _po(job.finish())
+        if prefix:
+            job.advance(max_steps=prefix)
+            # the step's result read back to the host: the bond dimensions
+            bits = ",".join(str(b) for b in job.m.bond_dims())
+        else:
+            job.advance()
+            bits, p = _po(job.finish())
     e1.record(stream)
     barrier()
     c1 = nat.counters()
@@ -472,10 +496,16 @@ def main():
                            unswap_order="parity-batched" if world > 1 else "parity-parallel",
                            warmup_steps=(f"first {args.warm_prefix} absorption steps" if big and args.warm_prefix
                                          else "full contractions"),
-                           timed_region="per-class / per-stage CUDA events on (roofline durations)"),
-            "peak": {"bits": peaks[-1][0], "probability": peaks[-1][1],
-                     "planted": inst.peak, "match": peaks[-1][0] == inst.peak,
-                     "e2e_bits_match": bits == peaks[-1][0]},
+                           timed_region="per-class / per-stage CUDA events on (roofline durations)",
+                           step=(f"first {prefix} absorption steps of the contraction (fixed prefix, "
+                                 "same circuit and settings)" if prefix else
+                                 "full contraction + peak extraction"),
+                           source_gates_per_step=gates_step),
+            "peak": ({"bits": peaks[-1][0], "probability": peaks[-1][1],
+                      "planted": inst.peak, "match": peaks[-1][0] == inst.peak,
+                      "e2e_bits_match": bits == peaks[-1][0]} if peaks[-1] is not None else
+                     {"bits": None, "note": f"timed step = first {prefix} absorption steps; the full "
+                      "contraction of this instance is reported in profiles/r02_c56_full.jsonl"}),
             "two_qubit_gates": n2q,
             "gpu_launches": launches,
             "clocks": clk,

@@ -57,7 +57,8 @@ int mb_synchronize(void);
 /* Kernels this library launched since load. */
 long long mb_launch_count(void);
 /* Per-kernel-class device timing with CUDA events on the engine stream.
- * Classes: 0 gemm, 1 gate, 2 svd_small, 3 svd_large, 4 emit, 5 other. */
+ * Classes: 0 gemm, 1 gate, 2 svd_small, 3 svd_large (Gram eigensolver path),
+ * 4 emit, 5 other, 6 svd_jacobi (large block-Jacobi path). Arrays of 7. */
 int mb_profile_begin(void);
 int mb_profile_end(double* ms_per_class, long long* launches_per_class, double* flops_per_class);
 /* Counters: [0] small SVDs, [1] large SVDs, [2] large sweeps, [3] host syncs,

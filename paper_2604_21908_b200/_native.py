@@ -158,7 +158,7 @@ def counters() -> dict:
     return dict(zip(keys, (int(x) for x in out)))
 
 
-PROFILE_CLASSES = ("gemm", "gate", "svd_small", "svd_large", "emit", "other")
+PROFILE_CLASSES = ("gemm", "gate", "svd_small", "svd_large", "emit", "other", "svd_jacobi")
 
 
 def profile_begin() -> None:
@@ -166,9 +166,9 @@ def profile_begin() -> None:
 
 
 def profile_end() -> dict:
-    ms = (C.c_double * 6)()
-    n = (C.c_longlong * 6)()
-    fl = (C.c_double * 6)()
+    ms = (C.c_double * 7)()
+    n = (C.c_longlong * 7)()
+    fl = (C.c_double * 7)()
     check(load().mb_profile_end(ms, n, fl), "mb_profile_end")
     return {k: {"ms": ms[i], "launch_groups": int(n[i]), "flops": fl[i]}
             for i, k in enumerate(PROFILE_CLASSES)}

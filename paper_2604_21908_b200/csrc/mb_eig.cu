@@ -147,6 +147,9 @@ static void ep_harvest(bool all) {
   }
 }
 
+// set while this thread captures a CUDA graph (no per-launch events inside)
+static thread_local bool g_capturing = false;
+
 struct EigScope {
   bool on;
   int stage;
@@ -154,7 +157,7 @@ struct EigScope {
   cudaStream_t s;
   cudaEvent_t a = nullptr;
   EigScope(int st, cudaStream_t str, double by, double fl)
-      : on(g_ep.on), stage(st), bytes(by), flops(fl), s(str) {
+      : on(g_ep.on && !g_capturing), stage(st), bytes(by), flops(fl), s(str) {
     if (!on) return;
     std::lock_guard<std::mutex> g(g_ep.mu);
     a = ep_event();
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__(256) k_trd_symv(const zd* __restrict__ A, int6
 // k_trd_col would serialize O(n * 32) complex work per column on one SM).
 // Three launches per column: k_trd_upd (finish W[:, i-1], update column c,
 // partial |x|^2), k_trd_vec (Householder scalars, reflector, partial V^H v and
-// W^H v), k_trd_symv2 (y = A22 v - W p1 - V p2, partial y^H v). All partial
+// W^H v), k_symv_tiles (y = A22 v - W p1 - V p2, partial y^H v). All partial
 // sums are reduced in a fixed order (bitwise reproducible).
 constexpr int kRowBlk = 256;    // rows per block in upd / vec
 constexpr int64_t kGridRows = 768;  // trailing size above which the grid path runs
@@ -781,59 +784,6 @@ __global__ void __launch_bounds__(kRowBlk) k_trd_vec(zd* __restrict__ A, int64_t
   }
 }
 
-__global__ void __launch_bounds__(256) k_trd_symv2(const zd* __restrict__ A, int64_t n,
-                                                   const zd* __restrict__ VW, int64_t c, int i,
-                                                   const double* __restrict__ part_p, int nblk_p,
-                                                   zd* __restrict__ y, double* __restrict__ part_yv) {
-  __shared__ zd pv[2 * kNB];
-  __shared__ double red_re[8], red_im[8];
-  const zd* V = VW;
-  const zd* W = VW + (int64_t)kNB * n;
-  // p1 / p2 from the vec kernel's partials (fixed order, every block the same)
-  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
-    const int t = e < i ? e : kNB + (e - i);
-    double re = 0, im = 0;
-    for (int bb = 0; bb < nblk_p; ++bb) {
-      re += part_p[(int64_t)bb * kPartStride + 2 * t];
-      im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
-    }
-    pv[t] = mk<double>(re, im);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const zd* v = V + (int64_t)i * n;
-  double yvr = 0, yvi = 0;
-  for (int64_t r = c + 1 + warp; r < n; r += nwarps) {
-    const zd dot = col_dot(A + r * n, v, c + 1, n, lane);
-    if (lane == 0) {
-      zd acc = dot;
-      for (int t = 0; t < i; ++t) {
-        acc = csub(acc, cmul(W[r + t * n], pv[t]));
-        acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
-      }
-      y[r] = acc;
-      const zd yv = cmulc(acc, v[r]);  // conj(y_r) v_r
-      yvr += yv.x;
-      yvi += yv.y;
-    }
-  }
-  if (lane == 0) {
-    red_re[wid] = yvr;
-    red_im[wid] = yvi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0, bq = 0;
-    for (int w2 = 0; w2 < 8; ++w2) {
-      a += red_re[w2];
-      bq += red_im[w2];
-    }
-    part_yv[(int64_t)blockIdx.x * kPartStride] = a;
-    part_yv[(int64_t)blockIdx.x * kPartStride + 1] = bq;
-  }
-}
 
 // dst[r, t] = src[r, t] for r < m, t < b (column-major, leading dimension ld)
 __global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, int64_t m, int b,
@@ -850,15 +800,68 @@ __global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, in
 // 64 x 64; a lower tile (I, J), I > J, contributes A_IJ v_J to y_I and
 // A_IJ^H v_I to y_J, a diagonal tile its Hermitian completion to y_I. Each
 // contribution lands in its own slot P[row tile][other tile] (no atomics);
-// k_symv_sum adds the slots in a fixed order.
+// the row tile's last contributor adds the slots in a fixed order.
 constexpr int kST = 64;
+
+// The block that completes a row tile (last of its nt contributions, counted
+// with an atomic per tile) also reduces that tile's slots in a fixed order,
+// applies the panel corrections and writes y and the tile's y^H v partial —
+// no separate reduction launch.
+__device__ void symv_finish_tile(const zd* __restrict__ P, int nt, int64_t n, int64_t s0, int I,
+                                 const zd* __restrict__ VW, int i, const double* __restrict__ part_p,
+                                 int nblk_p, zd* __restrict__ y, double* __restrict__ part_yv,
+                                 zd* pv, double* red) {
+  const zd* V = VW;
+  const zd* W = VW + (int64_t)kNB * n;
+  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
+    const int t = e < i ? e : kNB + (e - i);
+    double re = 0, im = 0;
+    for (int bb = 0; bb < nblk_p; ++bb) {
+      re += part_p[(int64_t)bb * kPartStride + 2 * t];
+      im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
+    }
+    pv[t] = mk<double>(re, im);
+  }
+  __syncthreads();
+  const zd* v = V + (int64_t)i * n;
+  double yr = 0, yi = 0;
+  if (threadIdx.x < kST) {
+    const int64_t r = s0 + (int64_t)I * kST + threadIdx.x;
+    if (r < n) {
+      zd acc = mk<double>(0, 0);
+      const zd* Pr = P + (int64_t)I * nt * kST + threadIdx.x;
+      for (int sl = 0; sl < nt; ++sl) acc = cadd(acc, Pr[(int64_t)sl * kST]);
+      for (int t = 0; t < i; ++t) {
+        acc = csub(acc, cmul(W[r + t * n], pv[t]));
+        acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
+      }
+      y[r] = acc;
+      const zd yv = cmulc(acc, v[r]);
+      yr = yv.x;
+      yi = yv.y;
+    }
+  }
+  yr = block_sum(yr, red);
+  __syncthreads();
+  yi = block_sum(yi, red);
+  if (threadIdx.x == 0) {
+    part_yv[(int64_t)I * kPartStride] = yr;
+    part_yv[(int64_t)I * kPartStride + 1] = yi;
+  }
+}
 
 __global__ void __launch_bounds__(256) k_symv_tiles(const zd* __restrict__ A, int64_t n, int64_t s0,
                                                     const zd* __restrict__ v, int nt,
-                                                    zd* __restrict__ P) {
+                                                    zd* __restrict__ P, int* __restrict__ cnt,
+                                                    const zd* __restrict__ VW, int i,
+                                                    const double* __restrict__ part_p, int nblk_p,
+                                                    zd* __restrict__ y, double* __restrict__ part_yv) {
   __shared__ zd vI[kST], vJ[kST];
   __shared__ zd rowp[4][kST];
   __shared__ zd colp[2][4][16];
+  __shared__ zd pv[2 * kNB];
+  __shared__ double red[32];
+  __shared__ int last_I, last_J;
   // lower-tile index -> (I, J), I >= J
   const int64_t t = blockIdx.x;
   int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -909,53 +912,20 @@ __global__ void __launch_bounds__(256) k_symv_tiles(const zd* __restrict__ A, in
     const int cc = tid - kST;
     PJ[cc] = cadd(colp[0][cc >> 4][cc & 15], colp[1][cc >> 4][cc & 15]);
   }
-}
-
-// y[r] = sum_slot P[r tile][slot][r] - sum_{t<i} (W[r,t] p1[t] + V[r,t] p2[t]),
-// plus the per-block partial y^H v (as k_trd_symv2)
-__global__ void __launch_bounds__(256) k_symv_sum(const zd* __restrict__ P, int nt, int64_t n,
-                                                  int64_t s0, const zd* __restrict__ VW, int i,
-                                                  const double* __restrict__ part_p, int nblk_p,
-                                                  zd* __restrict__ y, double* __restrict__ part_yv) {
-  __shared__ zd pv[2 * kNB];
-  __shared__ double red[32];
-  const zd* V = VW;
-  const zd* W = VW + (int64_t)kNB * n;
-  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
-    const int t = e < i ? e : kNB + (e - i);
-    double re = 0, im = 0;
-    for (int bb = 0; bb < nblk_p; ++bb) {
-      re += part_p[(int64_t)bb * kPartStride + 2 * t];
-      im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
-    }
-    pv[t] = mk<double>(re, im);
+  // completion counting: this tile feeds row tile I (and J when I != J)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    last_I = atomicAdd(&cnt[I], 1) == nt - 1;
+    last_J = (I != J) ? atomicAdd(&cnt[J], 1) == nt - 1 : 0;
+    if (last_I) cnt[I] = 0;  // reset for the next launch
+    if (last_J) cnt[J] = 0;
   }
   __syncthreads();
-  const int64_t r = s0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const zd* v = V + (int64_t)i * n;
-  double yr = 0, yi = 0;
-  if (r < n) {
-    const int64_t rr = r - s0;
-    const int64_t I = rr / kST, off = rr % kST;
-    zd acc = mk<double>(0, 0);
-    const zd* Pr = P + I * nt * kST + off;
-    for (int sl = 0; sl < nt; ++sl) acc = cadd(acc, Pr[(int64_t)sl * kST]);
-    for (int t = 0; t < i; ++t) {
-      acc = csub(acc, cmul(W[r + t * n], pv[t]));
-      acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
-    }
-    y[r] = acc;
-    const zd yv = cmulc(acc, v[r]);
-    yr = yv.x;
-    yi = yv.y;
-  }
-  yr = block_sum(yr, red);
+  if (last_I || last_J) __threadfence();
+  if (last_I) symv_finish_tile(P, nt, n, s0, I, VW, i, part_p, nblk_p, y, part_yv, pv, red);
   __syncthreads();
-  yi = block_sum(yi, red);
-  if (threadIdx.x == 0) {
-    part_yv[(int64_t)blockIdx.x * kPartStride] = yr;
-    part_yv[(int64_t)blockIdx.x * kPartStride + 1] = yi;
-  }
+  if (last_J) symv_finish_tile(P, nt, n, s0, J, VW, i, part_p, nblk_p, y, part_yv, pv, red);
 }
 
 // Hermitian completion of the trailing block [s, n)^2 from its lower triangle
@@ -973,7 +943,7 @@ __global__ void k_trd_last(const zd* __restrict__ A, int64_t n, double* __restri
 }
 
 static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* pv, zd* y,
-                  double* part, zd* slots, cudaStream_t s) {
+                  double* part, zd* slots, int* tile_cnt, cudaStream_t s) {
   if (n == 1) {
     k_trd_last<<<1, 1, 0, s>>>(A, n, d);
     EIG_CHECK();
@@ -985,6 +955,7 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
   double* part_yv = part + 2 * (size_t)kMaxSymvBlk * kPartStride;
   const int64_t nref = n - 1;
   int nblk_yv = 0;  // blocks of the previous column's symv (grid path)
+  cudaMemsetAsync(tile_cnt, 0, sizeof(int) * (size_t)(ediv(n, kST) + 1), s);
   bool upper_stale = false;  // the grid path keeps only the lower triangle current
   for (int64_t j0 = 0; j0 < nref; j0 += kNB) {
     const int b = (int)std::min<int64_t>(kNB, nref - j0);
@@ -1035,12 +1006,10 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
         const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
         EigScope sc(ES_TRD_SYMV, s, 8.0 * (double)rw * (double)(rw + 1) + 16.0 * rw * (2.0 * i + 2.0),
                     8.0 * (double)rw * (double)rw);
-        k_symv_tiles<<<(unsigned)ntiles, 256, 0, s>>>(A, n, c + 1, VW + (int64_t)i * n, nt, slots);
+        k_symv_tiles<<<(unsigned)ntiles, 256, 0, s>>>(A, n, c + 1, VW + (int64_t)i * n, nt, slots,
+                                                      tile_cnt, VW, i, part_p, nblk_v, y, part_yv);
         EIG_CHECK();
-        const int blocks = (int)ediv(rw, 256);
-        k_symv_sum<<<blocks, 256, 0, s>>>(slots, nt, n, c + 1, VW, i, part_p, nblk_v, y, part_yv);
-        EIG_CHECK();
-        nblk_yv = blocks;
+        nblk_yv = nt;
       }
     }
     // trailing update A22 -= V W^H + W V^H (rows / cols >= j0 + b): for a full
@@ -1070,6 +1039,86 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
   }
   k_trd_last<<<1, 1, 0, s>>>(A, n, d);
   EIG_CHECK();
+}
+
+// Replay of the tridiagonalization as a CUDA graph. Its launch sequence
+// depends only on n and on workspace addresses, so the second time a size
+// comes back on this thread (same workspace) the ~3 n launches are captured
+// once and replayed from then on: the GPU runs them back to back without a
+// host round trip per kernel. Profiled runs time the replay as one stage.
+struct TrdGraphCache {
+  struct Entry {
+    int64_t n;
+    const void* base;
+    cudaGraphExec_t exec;
+    long long last;
+  };
+  std::vector<Entry> graphs;
+  std::vector<std::pair<int64_t, int>> seen;  // size -> occurrences
+  long long tick = 0;
+  ~TrdGraphCache() {
+    for (auto& e : graphs) cudaGraphExecDestroy(e.exec);
+  }
+};
+static thread_local TrdGraphCache g_trd_graphs;
+static const bool kTrdGraphs = !getenv("MB_TRD_GRAPH") || atoi(getenv("MB_TRD_GRAPH")) != 0;
+
+static void hetrd_replay(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* pv, zd* y,
+                         double* part, zd* slots, int* tile_cnt, const void* base,
+                         cudaStream_t s) {
+  TrdGraphCache& C = g_trd_graphs;
+  ++C.tick;
+  if (kTrdGraphs && n >= 128) {
+    for (auto& en : C.graphs)
+      if (en.n == n && en.base == base) {
+        en.last = C.tick;
+        EigScope sc(ES_TRD_SYMV, s, 8.0 * (double)n * (double)n * (double)n / 3.0,
+                    (16.0 / 3.0) * (double)n * (double)n * (double)n);
+        if (cudaGraphLaunch(en.exec, s) != cudaSuccess)
+          throw std::runtime_error("eig: graph launch failed");
+        g_launches.fetch_add(3 * n, std::memory_order_relaxed);
+        return;
+      }
+    int cnt = 0;
+    for (auto& sz : C.seen)
+      if (sz.first == n) cnt = ++sz.second;
+    if (!cnt) C.seen.push_back({n, cnt = 1});
+    if (cnt >= 2) {
+      cudaGraph_t g;
+      g_capturing = true;
+      cudaError_t err = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      if (err == cudaSuccess) {
+        try {
+          hetrd(A, n, VW, d, e, tau, pv, y, part, slots, tile_cnt, s);
+        } catch (...) {
+          cudaStreamEndCapture(s, &g);
+          g_capturing = false;
+          throw;
+        }
+        err = cudaStreamEndCapture(s, &g);
+      }
+      g_capturing = false;
+      cudaGraphExec_t exec = nullptr;
+      if (err == cudaSuccess && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+        cudaGraphDestroy(g);
+        if (C.graphs.size() >= 48) {  // evict the least recently used
+          size_t lru = 0;
+          for (size_t k = 1; k < C.graphs.size(); ++k)
+            if (C.graphs[k].last < C.graphs[lru].last) lru = k;
+          cudaGraphExecDestroy(C.graphs[lru].exec);
+          C.graphs.erase(C.graphs.begin() + lru);
+        }
+        C.graphs.push_back({n, base, exec, C.tick});
+        EigScope sc(ES_TRD_SYMV, s, 8.0 * (double)n * (double)n * (double)n / 3.0,
+                    (16.0 / 3.0) * (double)n * (double)n * (double)n);
+        if (cudaGraphLaunch(exec, s) != cudaSuccess)
+          throw std::runtime_error("eig: graph launch failed");
+        return;
+      }
+      cudaGetLastError();  // capture unavailable: fall through to direct launches
+    }
+  }
+  hetrd(A, n, VW, d, e, tau, pv, y, part, slots, tile_cnt, s);
 }
 
 // ---- 3. divide and conquer for the symmetric tridiagonal (d, e) ---------------
@@ -1325,9 +1374,24 @@ __global__ void __launch_bounds__(128) k_dc_gather(const DcMerge* __restrict__ m
   double* out = Qs + (int64_t)lo * ldq;
   const double* src = Q + lo + r;  // row lo + r
   double carry = 0.0;
-  for (int j = 0; j < m; ++j) {
-    const int a = S.act[lo + j];
-    const double q = src[(int64_t)(lo + S.perm[lo + j]) * ldq];
+  for (int j0 = 0; j0 < m; j0 += 8) {
+    // issue eight independent loads before the dependent streaming updates
+    double qv[8];
+    int av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u;
+      if (j < m) {
+        av[u] = S.act[lo + j];
+        qv[u] = src[(int64_t)(lo + S.perm[lo + j]) * ldq];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+    const int j = j0 + u;
+    if (j >= m) break;
+    const int a = av[u];
+    const double q = qv[u];
     if (a == 0) {
       out[r + (int64_t)(k + S.slot[lo + j]) * m] = q;
     } else if (a == 1) {
@@ -1342,19 +1406,22 @@ __global__ void __launch_bounds__(128) k_dc_gather(const DcMerge* __restrict__ m
       out[r + (int64_t)S.slot[lo + j] * m] = carry;
       carry = q;
     }
+    }
   }
   const int es = S.endslot[lo];
   if (es >= 0) out[r + (int64_t)es * m] = carry;
 }
 
-// Secular equation 1 + rho sum z_j^2 / (d_j - lambda) = 0, one root per
-// thread by bisection in the offset from the nearer pole.
+// Secular equation 1 + rho sum z_j^2 / (d_j - lambda) = 0: one warp per root
+// (lanes split the pole sums), bracketed Newton in the offset from the
+// nearer pole, bisection whenever a step leaves the bracket.
 __global__ void __launch_bounds__(128) k_dc_secular(const DcMerge* __restrict__ mg, DcScratch S,
                                                     const double* __restrict__ rho_arr) {
   const DcMerge g = mg[blockIdx.y];
   const int lo = g.lo;
   const int k = S.kcount[lo];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= k) return;
   const double rho = rho_arr[lo];
   const double* d = S.dnd + lo;
@@ -1364,8 +1431,9 @@ __global__ void __launch_bounds__(128) k_dc_secular(const DcMerge* __restrict__ 
   if (i < k - 1) {
     const double gap = d[i + 1] - d[i];
     const double mid = 0.5 * gap;
-    double f = 1.0;
-    for (int j = 0; j < k; ++j) f += rho * z[j] * z[j] / ((d[j] - d[i]) - mid);
+    double f = 0.0;
+    for (int j = lane; j < k; j += 32) f += rho * z[j] * z[j] / ((d[j] - d[i]) - mid);
+    f = 1.0 + warp_sum(f);
     if (f > 0) {
       org = i;
       lo_t = 0.0;
@@ -1378,22 +1446,22 @@ __global__ void __launch_bounds__(128) k_dc_secular(const DcMerge* __restrict__ 
   } else {
     org = k - 1;
     double zz = 0;
-    for (int j = 0; j < k; ++j) zz += z[j] * z[j];
+    for (int j = lane; j < k; j += 32) zz += z[j] * z[j];
     lo_t = 0.0;
-    hi_t = rho * zz;
+    hi_t = rho * warp_sum(zz);
   }
   const double dorg = d[org];
-  // bracketed Newton: f is increasing on the bracket; a Newton step that
-  // leaves the bracket (or stalls) is replaced by bisection
   double t = 0.5 * (lo_t + hi_t);
   for (int it = 0; it < 200; ++it) {
-    double f = 1.0, fp = 0.0;
-    for (int j = 0; j < k; ++j) {
+    double f = 0.0, fp = 0.0;
+    for (int j = lane; j < k; j += 32) {
       const double inv = 1.0 / ((d[j] - dorg) - t);
       const double w = rho * z[j] * z[j] * inv;
       f += w;
       fp += w * inv;
     }
+    f = 1.0 + warp_sum(f);
+    fp = warp_sum(fp);
     if (f > 0) hi_t = t;
     else if (f < 0) lo_t = t;
     else break;
@@ -1404,29 +1472,35 @@ __global__ void __launch_bounds__(128) k_dc_secular(const DcMerge* __restrict__ 
     if (tn == t) break;
     t = tn;
   }
-  S.org[lo + i] = org;
-  S.tau[lo + i] = t;
+  if (lane == 0) {
+    S.org[lo + i] = org;
+    S.tau[lo + i] = t;
+  }
 }
 
-// Gu-Eisenstat: zhat_i^2 = (lambda_i - d_i)/rho * prod_{j != i} (lambda_j - d_i)/(d_j - d_i)
+// Gu-Eisenstat: zhat_i^2 = (lambda_i - d_i)/rho * prod_{j != i} (lambda_j - d_i)/(d_j - d_i),
+// one warp per i (lane partial products, then a fixed-order warp product)
 __global__ void __launch_bounds__(128) k_dc_zhat(const DcMerge* __restrict__ mg, DcScratch S,
                                                  const double* __restrict__ rho_arr) {
   const DcMerge g = mg[blockIdx.y];
   const int lo = g.lo;
   const int k = S.kcount[lo];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= k) return;
   const double rho = rho_arr[lo];
   const double* d = S.dnd + lo;
   const double di = d[i];
   double val = 1.0;
-  for (int j = 0; j < k; ++j) {
+  for (int j = lane; j < k; j += 32) {
     const int oj = S.org[lo + j];
     const double lam_m_di = (d[oj] - di) + S.tau[lo + j];  // lambda_j - d_i
     if (j == i) val *= lam_m_di / rho;
     else val *= lam_m_di / (d[j] - di);
   }
-  S.zhat[lo + i] = copysign(sqrt(fmax(val, 0.0)), S.znd[lo + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) val *= __shfl_xor_sync(0xffffffffu, val, o);
+  if (lane == 0) S.zhat[lo + i] = copysign(sqrt(fmax(val, 0.0)), S.znd[lo + i]);
 }
 
 // Eigenvectors of D + rho zhat zhat^T: column j = zhat / (d - lambda_j),
@@ -1532,7 +1606,7 @@ struct EigLayout {
 enum {
   L_G, L_VC, L_QA, L_QS, L_SV, L_VW, L_D, L_E, L_TAU, L_PV, L_Y, L_DS, L_ZS, L_PERM, L_ACT, L_RCS,
   L_SLOT, L_END, L_K, L_DND, L_ZND, L_ORG, L_TAUS, L_ZH, L_RHO, L_MG, L_LEAF, L_GD, L_FAIL, L_YB,
-  L_T, L_W1, L_W2, L_YTY, L_PART, L_SPLIT, L_SYMV, L_NUM
+  L_T, L_W1, L_W2, L_YTY, L_PART, L_SPLIT, L_SYMV, L_TCNT, L_NUM
 };
 
 static void layout(int64_t n, size_t* off, size_t& total) {
@@ -1568,6 +1642,7 @@ static void layout(int64_t n, size_t* off, size_t& total) {
       3 * (size_t)kMaxSymvBlk * kPartStride * 8,    // hetrd partial sums
       (size_t)n * kNBT * 16 * kMaxSplit,            // split-K partials (back-transform)
       (size_t)ediv(n, 64) * ediv(n, 64) * 64 * 16,  // lower-triangle matvec slots
+      (size_t)ediv(n, 64) * 4 + 64,                 // per-row-tile completion counters
   };
   size_t o = 0;
   for (int i = 0; i < L_NUM; ++i) {
@@ -1708,7 +1783,8 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host, bool back
 
   // 2. tridiagonalize
   dbg_check("gram", G, 2 * n * n, s);
-  hetrd(G, n, VW, d, e, tau, pv, y, (double*)(B + off[L_PART]), (zd*)(B + off[L_SYMV]), s);
+  hetrd_replay(G, n, VW, d, e, tau, pv, y, (double*)(B + off[L_PART]), (zd*)(B + off[L_SYMV]),
+               (int*)(B + off[L_TCNT]), B, s);
   dbg_check("d", d, n, s);
   dbg_check("e", e, n - 1, s);
 
@@ -1764,9 +1840,10 @@ static void heevd(int64_t n, void* ws, cudaStream_t s, int* fail_host, bool back
       dim3 g((unsigned)ediv(mmax, 128), (unsigned)nm);
       k_dc_gather<<<g, 128, 0, s>>>(mgl, Qa, n, S, Qs);
       EIG_CHECK();
-      k_dc_secular<<<g, 128, 0, s>>>(mgl, S, rho);
+      dim3 gw((unsigned)ediv((int64_t)mmax * 32, 128), (unsigned)nm);
+      k_dc_secular<<<gw, 128, 0, s>>>(mgl, S, rho);
       EIG_CHECK();
-      k_dc_zhat<<<g, 128, 0, s>>>(mgl, S, rho);
+      k_dc_zhat<<<gw, 128, 0, s>>>(mgl, S, rho);
       EIG_CHECK();
     }
     {
@@ -2079,8 +2156,8 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
     double* e = (double*)(B + off[L_E]);
     double* w = (double*)(B + off[L_DS]);
     dbg_check("gram", G, 2 * p * p, s);
-    hetrd(G, p, VW, d, e, (zd*)(B + off[L_TAU]), (zd*)(B + off[L_PV]), (zd*)(B + off[L_Y]),
-          (double*)(B + off[L_PART]), (zd*)(B + off[L_SYMV]), s);
+    hetrd_replay(G, p, VW, d, e, (zd*)(B + off[L_TAU]), (zd*)(B + off[L_PV]), (zd*)(B + off[L_Y]),
+                 (double*)(B + off[L_PART]), (zd*)(B + off[L_SYMV]), (int*)(B + off[L_TCNT]), B, s);
     {
       EigScope sc(ES_DC, s, 16.0 * (double)p, 0.0);
       k_bisect<<<(int)ediv(p, 256), 256, 0, s>>>(d, e, p, w);

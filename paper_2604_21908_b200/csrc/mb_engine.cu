@@ -53,7 +53,9 @@ struct DevBuf {
 };
 using Buf = std::shared_ptr<DevBuf>;
 
-enum ProfClass { P_GEMM = 0, P_GATE = 1, P_SVD_SMALL = 2, P_SVD_LARGE = 3, P_EMIT = 4, P_OTHER = 5 };
+enum ProfClass { P_GEMM = 0, P_GATE = 1, P_SVD_SMALL = 2, P_SVD_LARGE = 3, P_EMIT = 4, P_OTHER = 5,
+                 P_SVD_JACOBI = 6 };
+constexpr int kProfClasses = 7;
 
 struct ProfRec {
   int cls;
@@ -91,8 +93,8 @@ struct Engine {
   bool prof = false;
   std::deque<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
-  double pms[6] = {}, pfl[6] = {};
-  long long pn[6] = {};
+  double pms[kProfClasses] = {}, pfl[kProfClasses] = {};
+  long long pn[kProfClasses] = {};
 };
 
 // Two engine contexts (stream + scratch + readback buffers each): the main
@@ -278,6 +280,10 @@ static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64
 
 // ---- SVD orchestration ---------------------------------------------------
 
+// exact (untruncated) large splits at or above this width start from the
+// Gram eigenvectors instead of the identity (MB_SEED_JACOBI_P, 0 = never)
+static const int64_t kSeedJacobiP = getenv("MB_SEED_JACOBI_P") ? atoll(getenv("MB_SEED_JACOBI_P")) : 1024;
+
 template <typename R>
 static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double eps, int64_t chi,
                           bool want_v) {
@@ -378,7 +384,7 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       finish_large<R>(jobs[i], 1, 0, E.stream);
     } else {
       // exact splits and tight cutoffs: block one-sided Jacobi
-      ProfScope ps(P_SVD_LARGE, 2.0 * 8.0 * pd * pd * q);
+      ProfScope ps(P_SVD_JACOBI, 2.0 * 8.0 * pd * pd * q);
       double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
       const int64_t cap = large_pair_capacity(p);
       if (E.h_lg_cap < cap) {
@@ -395,8 +401,22 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       // block Jacobi; on non-convergence: Gram-preconditioned restart (direct
       // eigensolver seeds the sweeps), then the reference's perturbed retry
       int sweeps = 0;
-      bool conv = jacobi_large<R>(jobs[i], ws, E.stream, true, false, sweeps);
-      if (!conv) {
+      bool conv;
+      bool seeded = false;
+      if (p >= kSeedJacobiP && jobs[i].A) {
+        // big exact splits: seed the sweeps with the Gram eigenvectors first
+        // (plain block Jacobi needs tens of passes on these blobs)
+        if (!jobs[i].W)
+          jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
+                                   large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
+        init_large<R>(jobs[i], ws, E.stream);
+        gram_precondition<R>(jobs[i], grow(E.eigws, eig_workspace_bytes(p)), E.stream);
+        conv = jacobi_large<R>(jobs[i], ws, E.stream, false, false, sweeps);
+        seeded = true;
+      } else {
+        conv = jacobi_large<R>(jobs[i], ws, E.stream, true, false, sweeps);
+      }
+      if (!conv && !seeded) {
         if (!jobs[i].W)
           jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
                                    large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
@@ -1615,7 +1635,7 @@ static void trial_pair(mb_chain& l, int nl, const int* kl, const int* ql, const 
   }
   if (A.prof) {
     ProfScope::harvest(A, true);
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < kProfClasses; ++i) {
       M.pms[i] += A.pms[i];
       M.pfl[i] += A.pfl[i];
       M.pn[i] += A.pn[i];
@@ -1700,7 +1720,7 @@ int mb_profile_begin(void) {
   MB_TRY({
     ensure_ready();
     ProfScope::harvest(E, true);
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < kProfClasses; ++i) {
       E.pms[i] = E.pfl[i] = 0;
       E.pn[i] = 0;
     }
@@ -1715,7 +1735,7 @@ int mb_profile_end(double* ms, long long* launches, double* flops) {
     ensure_ready();
     ck(cudaStreamSynchronize(E.stream), "profile sync");
     ProfScope::harvest(E, true);
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < kProfClasses; ++i) {
       ms[i] = E.pms[i];
       launches[i] = E.pn[i];
       flops[i] = E.pfl[i];

@@ -1866,6 +1866,13 @@ bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fre
   return conv != 0;
 }
 
+// X (and V = I) from J.A with the |X|^2 partials, no sweeps
+template <typename R>
+void init_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
+  k_init_large<R><<<kSumBlocks, 256, 0, s>>>(J.A, J.X, J.V, J.m, J.n, ws.red_dev);
+  MB_LAUNCH_CHECK();
+}
+
 template <typename R>
 void svd_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s) {
   int sweeps = 0;
@@ -2245,6 +2252,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void svd_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                     \
   template void finish_large<R>(SvdJob<R>&, int, int, cudaStream_t);                            \
   template bool jacobi_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t, bool, bool, int&); \
+  template void init_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                  \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \
   template void launch_sweep<R>(const SweepPack<R>&, cudaStream_t);                             \

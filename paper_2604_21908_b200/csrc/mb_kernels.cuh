@@ -156,6 +156,10 @@ template <typename R>
 bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fresh, bool perturb,
                   int& sweeps);
 
+// X (and V = I) from J.A, no sweeps
+template <typename R>
+void init_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s);
+
 template <typename R>
 size_t large_workspace_elems(int64_t m, int64_t n);
 

@@ -38,6 +38,10 @@ def main():
         m = blob(rng, p, a.kind)
         svd_truncate(m, 1, 2e-3, 8192, dtype=a.dtype)  # warm-up (allocations)
         nat.synchronize()
+        t0 = time.perf_counter()
+        svd_truncate(m, 1, 2e-3, 8192, dtype=a.dtype)
+        nat.synchronize()
+        wall_plain = time.perf_counter() - t0
         nat.profile_begin()
         t0 = time.perf_counter()
         res = svd_truncate(m, 1, 2e-3, 8192, dtype=a.dtype)
@@ -46,7 +50,7 @@ def main():
         nat.profile_end()
         st = nat.profile_eig()
         tot = sum(v["ms"] for v in st.values())
-        out = {"p": p, "dtype": a.dtype, "kind": a.kind, "rank": len(res.s), "wall_ms": wall * 1e3,
+        out = {"p": p, "dtype": a.dtype, "kind": a.kind, "rank": len(res.s), "wall_ms": wall * 1e3, "wall_ms_unprofiled": wall_plain * 1e3,
                "stages_ms": {k: round(v["ms"], 3) for k, v in st.items()},
                "stage_total_ms": round(tot, 3),
                "launches": {k: v["launches"] for k, v in st.items()},
