@@ -824,13 +824,31 @@ __device__ void symv_finish_tile(const zd* __restrict__ P, int nt, int64_t n, in
   }
   __syncthreads();
   const zd* v = V + (int64_t)i * n;
+  // slot sums: four threads per row, each a contiguous quarter of the slots
+  // with four loads in flight, combined in a fixed order
+  __shared__ zd quarter[4][kST];
+  {
+    const int row = threadIdx.x & (kST - 1), qtr = threadIdx.x >> 6;
+    const int per = (nt + 3) / 4, s_lo = qtr * per, s_hi = min(nt, s_lo + per);
+    const zd* Pr = P + (int64_t)I * nt * kST + row;
+    zd a0 = mk<double>(0, 0), a1 = a0, a2 = a0, a3 = a0;
+    int sl = s_lo;
+    for (; sl + 3 < s_hi; sl += 4) {
+      a0 = cadd(a0, Pr[(int64_t)sl * kST]);
+      a1 = cadd(a1, Pr[(int64_t)(sl + 1) * kST]);
+      a2 = cadd(a2, Pr[(int64_t)(sl + 2) * kST]);
+      a3 = cadd(a3, Pr[(int64_t)(sl + 3) * kST]);
+    }
+    for (; sl < s_hi; ++sl) a0 = cadd(a0, Pr[(int64_t)sl * kST]);
+    quarter[qtr][row] = cadd(cadd(a0, a1), cadd(a2, a3));
+  }
+  __syncthreads();
   double yr = 0, yi = 0;
   if (threadIdx.x < kST) {
     const int64_t r = s0 + (int64_t)I * kST + threadIdx.x;
     if (r < n) {
-      zd acc = mk<double>(0, 0);
-      const zd* Pr = P + (int64_t)I * nt * kST + threadIdx.x;
-      for (int sl = 0; sl < nt; ++sl) acc = cadd(acc, Pr[(int64_t)sl * kST]);
+      zd acc = cadd(cadd(quarter[0][threadIdx.x], quarter[1][threadIdx.x]),
+                    cadd(quarter[2][threadIdx.x], quarter[3][threadIdx.x]));
       for (int t = 0; t < i; ++t) {
         acc = csub(acc, cmul(W[r + t * n], pv[t]));
         acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
