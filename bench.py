@@ -264,13 +264,14 @@ def run_reference(args, rank, world):
 
 # the kernel behind each large-SVD stage (mb_eig.cu) and its bound
 _STAGE_KERNEL = {
-    "trd_symv": ("k_symv_tiles (tridiagonalization, CUDA graph)", "hbm"),
-    "trd_panel": ("k_trd_upd/k_trd_vec", "latency"),
-    "trd_update": ("k_gemm_cm<zd,zd,N,C>", "fp64"),
-    "gram": ("k_gemm_cm<cx,zd,C,N>", "fp64"),
-    "backtransform": ("k_gemm_cm<zd,zd,*,*>", "fp64"),
-    "xv": ("k_gemm_cm<cx,cx,N,N>", "fp64"),
-    "dc": ("k_dc_*", "latency"),
+    # stage: (kernel, bound, key in profiles/r02_kernel_traffic.json)
+    "trd_symv": ("k_symv_tiles2 + k_trd_upd2 (tridiagonalization, CUDA graph)", "hbm", "k_symv_tiles"),
+    "trd_panel": ("k_trd_upd2", "latency", "k_trd_upd"),
+    "trd_update": ("k_gemm_cm<zd,zd,N,C>", "fp64", "k_gemm_cm"),
+    "gram": ("k_gemm_cm<cx,zd,C,N>", "fp64", "k_gemm_cm"),
+    "backtransform": ("k_gemm_cm<zd,zd,*,*>", "fp64", "k_gemm_cm"),
+    "xv": ("k_gemm_cm<cx,cx,N,N>", "fp64", "k_gemm_cm"),
+    "dc": ("k_dc_*", "latency", None),
 }
 
 
@@ -321,7 +322,7 @@ def _roofline(prof, stages, hbm, src, fp64, dev_ms):
                 "unit": None, "frac": None, "traffic": None,
                 "share_of_profiled_device_time": d["ms"] / tot,
                 "note": "no large-SVD stage ran; small dependent factorizations (latency-bound)"}
-    kernel, bound = _STAGE_KERNEL[name]
+    kernel, bound, tkey = _STAGE_KERNEL[name]
     traffic = _stage_traffic()
     out = {"kernel": kernel, "stage": name, "launches": st["launches"],
            "ms_total": round(st["ms"], 3),
@@ -330,8 +331,7 @@ def _roofline(prof, stages, hbm, src, fp64, dev_ms):
            "share_of_step": st["ms"] / dev_ms if dev_ms else None,
            "algorithmic_bytes_per_launch": st["bytes"] / max(st["launches"], 1),
            "algorithmic_flops_per_launch": st["flops"] / max(st["launches"], 1),
-           "traffic": (traffic or {}).get(kernel.split("/")[0], {}).get("dram_bytes_per_launch")
-           if traffic else None,
+           "traffic": ((traffic or {}).get("kernels", {}).get(tkey, {}) if tkey else {}) or None,
            "traffic_source": "profiles/r02_kernel_traffic.json (ncu --set full)" if traffic else None}
     if bound == "hbm" or bound == "latency":
         ach = st["bytes"] / (st["ms"] / 1e3) / 1e9 if st["ms"] else 0.0

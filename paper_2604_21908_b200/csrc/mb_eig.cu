@@ -216,7 +216,7 @@ struct GemmDesc {
 constexpr int TBM = 64, TBN = 64;
 
 template <typename TI, typename TC, bool CA, bool CB, int BK>
-__global__ void __launch_bounds__(256) k_gemm_cm(const GemmDesc* __restrict__ descs, GemmDesc one,
+__global__ void __launch_bounds__(256, 2) k_gemm_cm(const GemmDesc* __restrict__ descs, GemmDesc one,
                                                  double alpha, double beta, int64_t kslice,
                                                  int lower = 0) {
   __shared__ TC As[BK][TBM + 1];
@@ -946,6 +946,298 @@ __global__ void __launch_bounds__(256) k_symv_tiles(const zd* __restrict__ A, in
   if (last_J) symv_finish_tile(P, nt, n, s0, J, VW, i, part_p, nblk_p, y, part_yv, pv, red);
 }
 
+// ---- fused panel step (grid path): two launches per column --------------------
+//
+// k_trd_upd2 finishes the previous column's w (its matvec arrives raw; the
+// panel corrections -W p1 - V p2 and alpha are applied here from the tile
+// kernel's partials), stores the previous reflector into A, and updates
+// column c. k_symv_tiles2 derives the Householder scalars of column c from
+// the update's partial norms in every block, forms v on the fly, multiplies
+// the trailing block (lower triangle), and its diagonal tiles publish V[:, i]
+// and the partial V^H v, W^H v. All partial sums are reduced in fixed order.
+
+// y_r - sum_{t < nt_} (W[r,t] p1[t] + V[r,t] p2[t]) with batched loads
+__device__ __forceinline__ zd row_corrected(zd yr, const zd* __restrict__ V, const zd* __restrict__ W,
+                                           int64_t r, int64_t n, int nt_, const zd* pv) {
+  for (int t0 = 0; t0 < nt_; t0 += 8) {
+    zd vv[8], ww[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < nt_) {
+        vv[u] = V[r + (t0 + u) * n];
+        ww[u] = W[r + (t0 + u) * n];
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < nt_) {
+        yr = csub(yr, cmul(ww[u], pv[t0 + u]));
+        yr = csub(yr, cmul(vv[u], pv[kNB + t0 + u]));
+      }
+  }
+  return yr;
+}
+
+__global__ void __launch_bounds__(kRowBlk) k_trd_upd2(zd* __restrict__ A, int64_t n,
+                                                      zd* __restrict__ VW, int64_t j0, int i, int b,
+                                                      double* __restrict__ dd, const zd* __restrict__ tau,
+                                                      const zd* __restrict__ y,
+                                                      const double* __restrict__ part_yv,
+                                                      const double* __restrict__ part_p, int nt_prev,
+                                                      double* __restrict__ part_x) {
+  __shared__ zd sh_rowv[kNB], sh_roww[kNB];
+  __shared__ zd pv[2 * kNB];
+  __shared__ zd sh_alpha;
+  __shared__ double red[32];
+  zd* V = VW;
+  zd* W = VW + (int64_t)kNB * n;
+  const int64_t c = j0 + i;  // column to update (if i < b); previous column c - 1
+  const int64_t r = c + (int64_t)blockIdx.x * kRowBlk + threadIdx.x;
+  const int tp_i = i - 1;  // panel index of the previous column
+  zd tp = mk<double>(0, 0);
+  if (i > 0) {
+    tp = tau[c - 1];
+    // p1 = V^H v, p2 = W^H v of the previous column (t < i - 1), per row tile
+    for (int e = threadIdx.x; e < 2 * tp_i; e += blockDim.x) {
+      const int t = e < tp_i ? e : kNB + (e - tp_i);
+      double re = 0, im = 0;
+      for (int bb = 0; bb < nt_prev; ++bb) {
+        re += part_p[(int64_t)bb * kPartStride + 2 * t];
+        im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
+      }
+      pv[t] = mk<double>(re, im);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      zd yv = fixed_sum_cx(part_yv, nt_prev, 0);  // sum conj(y_raw) v
+      if (threadIdx.x == 0) {
+        // the corrections' share: sum_t conj(p1_t) p2_t + conj(p2_t) p1_t
+        for (int t = 0; t < tp_i; ++t) {
+          yv = csub(yv, cmulc(pv[t], pv[kNB + t]));
+          yv = csub(yv, cmulc(pv[kNB + t], pv[t]));
+        }
+        // alpha = -tau/2 (w^H v), w = tau y  =>  w^H v = conj(tau) (y^H v)
+        sh_alpha = cmul(mk<double>(-0.5 * tp.x, -0.5 * tp.y), cmul(cconj(tp), yv));
+      }
+    }
+    __syncthreads();
+  }
+  const zd al = i > 0 ? sh_alpha : mk<double>(0, 0);
+  zd wr = mk<double>(0, 0);
+  if (i > 0 && r < n) {
+    const zd vr = V[r + tp_i * n];
+    const zd yc = row_corrected(y[r], V, W, r, n, tp_i, pv);
+    wr = cadd(cmul(tp, yc), cmul(al, vr));
+    W[r + tp_i * n] = wr;
+    if (r >= c + 1) A[r + (c - 1) * n] = vr;  // the previous reflector, for the back-transform
+  }
+  if (i >= b) return;
+  if (threadIdx.x < i) {
+    const int t = threadIdx.x;
+    sh_rowv[t] = V[c + t * n];
+    if (t == tp_i) {
+      const zd yc = row_corrected(y[c], V, W, c, n, tp_i, pv);
+      sh_roww[t] = cadd(cmul(tp, yc), cmul(al, V[c + t * n]));
+    } else {
+      sh_roww[t] = W[c + t * n];
+    }
+  }
+  __syncthreads();
+  double xn = 0;
+  if (r < n) {
+    const zd a = panel_row_update(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, tp_i, wr);
+    A[r + c * n] = a;
+    if (r == c) dd[c] = a.x;
+    if (r >= c + 2) xn = cabs2(a);
+  }
+  xn = block_sum(xn, red);
+  if (threadIdx.x == 0) part_x[(int64_t)blockIdx.x * kPartStride] = xn;
+}
+
+__device__ __forceinline__ zd vload(const zd* __restrict__ A, int64_t n, int64_t c, int64_t r, zd sc) {
+  if (r >= n) return mk<double>(0, 0);
+  if (r == c + 1) return mk<double>(1, 0);
+  return cmul(A[r + c * n], sc);
+}
+
+__global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, int64_t n, int64_t c,
+                                                     zd* __restrict__ VW, int i, int nt,
+                                                     zd* __restrict__ P, int* __restrict__ cnt,
+                                                     const double* __restrict__ part_x, int nblk_x,
+                                                     double* __restrict__ ee, zd* __restrict__ tau,
+                                                     zd* __restrict__ y, double* __restrict__ part_yv,
+                                                     double* __restrict__ part_p) {
+  __shared__ zd vI[kST], vJ[kST];
+  __shared__ zd rowp[4][kST];
+  __shared__ zd colp[2][4][16];
+  __shared__ zd quarter[4][kST];
+  __shared__ zd sh_sc;
+  __shared__ zd red_w[2][2 * kNB];
+  __shared__ double red[32];
+  __shared__ int last_I, last_J;
+  zd* V = VW;
+  const zd* W = VW + (int64_t)kNB * n;
+  const int64_t s0 = c + 1;
+  const int tid = threadIdx.x;
+  // Householder scalars of column c (zlarfg), identical in every block
+  if (tid < 32) {
+    double x = 0;
+    for (int bb = tid; bb < nblk_x; bb += 32) x += part_x[(int64_t)bb * kPartStride];
+    x = warp_sum(x);
+    if (tid == 0) {
+      const zd al = A[(c + 1) + c * n];
+      zd tv, sc;
+      double beta;
+      if (x + al.x * al.x + al.y * al.y < 1e-250) {
+        tv = mk<double>(0, 0);
+        beta = al.x;
+        sc = mk<double>(0, 0);
+      } else {
+        beta = -copysign(sqrt(al.x * al.x + al.y * al.y + x), al.x);
+        tv = mk<double>((beta - al.x) / beta, -al.y / beta);
+        const zd den = mk<double>(al.x - beta, al.y);
+        const double dn = den.x * den.x + den.y * den.y;
+        sc = mk<double>(den.x / dn, -den.y / dn);
+      }
+      sh_sc = sc;
+      if (blockIdx.x == 0) {
+        ee[c] = beta;
+        tau[c] = tv;
+      }
+    }
+  }
+  __syncthreads();
+  const zd sc = sh_sc;
+  const int64_t t = blockIdx.x;
+  int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= t) ++I;
+  while ((int64_t)I * (I + 1) / 2 > t) --I;
+  const int J = (int)(t - (int64_t)I * (I + 1) / 2);
+  const int tr = tid & 63, tg = tid >> 6;
+  const int64_t r0 = s0 + (int64_t)I * kST, c0 = s0 + (int64_t)J * kST;
+  if (tid < kST) {
+    vI[tid] = vload(A, n, c, r0 + tid, sc);
+    vJ[tid] = vload(A, n, c, c0 + tid, sc);
+  }
+  __syncthreads();
+  const int64_t r = r0 + tr;
+  zd a[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int cc = tg * 16 + u;
+    const int64_t cg = c0 + cc;
+    a[u] = (r < n && cg < n && (I != J || tr >= cc)) ? A[r + cg * n] : mk<double>(0, 0);
+  }
+  zd acc = mk<double>(0, 0);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc = cadd(acc, cmul(a[u], vJ[tg * 16 + u]));
+  rowp[tg][tr] = acc;
+  const int lane = tid & 31, half = (tid >> 5) & 1;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int cc = tg * 16 + u;
+    zd x = (I != J || tr > cc) ? cmulc(a[u], vI[tr]) : mk<double>(0, 0);
+    x.x = warp_sum(x.x);
+    x.y = warp_sum(x.y);
+    if (lane == 0) colp[half][tg][u] = x;
+  }
+  // diagonal tiles publish v and the partial V^H v, W^H v of their rows
+  if (I == J && tid < kST) {
+    const int64_t rr = r0 + tid;
+    const zd vr = vI[tid];
+    if (rr < n) V[rr + (int64_t)i * n] = vr;
+    for (int t0 = 0; t0 < i; t0 += 8) {
+      zd va[8], wa[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        va[u] = mk<double>(0, 0);
+        wa[u] = mk<double>(0, 0);
+        if (rr < n && t0 + u < i) {
+          va[u] = cmulc(V[rr + (t0 + u) * n], vr);
+          wa[u] = cmulc(W[rr + (t0 + u) * n], vr);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (t0 + u >= i) break;
+        const double ar = warp_sum(va[u].x), ai = warp_sum(va[u].y);
+        const double wr = warp_sum(wa[u].x), wi = warp_sum(wa[u].y);
+        if (lane == 0) {
+          red_w[tid >> 5][t0 + u] = mk<double>(ar, ai);
+          red_w[tid >> 5][kNB + t0 + u] = mk<double>(wr, wi);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (I == J)
+    for (int e = tid; e < 2 * i; e += blockDim.x) {
+      const int tt = e < i ? e : kNB + (e - i);
+      const zd sum = cadd(red_w[0][tt], red_w[1][tt]);
+      part_p[(int64_t)I * kPartStride + 2 * tt] = sum.x;
+      part_p[(int64_t)I * kPartStride + 2 * tt + 1] = sum.y;
+    }
+  zd* PI = P + ((int64_t)I * nt + J) * kST;
+  zd* PJ = P + ((int64_t)J * nt + I) * kST;
+  if (tid < kST) {
+    zd yv = cadd(cadd(rowp[0][tid], rowp[1][tid]), cadd(rowp[2][tid], rowp[3][tid]));
+    if (I == J) yv = cadd(yv, cadd(colp[0][tid >> 4][tid & 15], colp[1][tid >> 4][tid & 15]));
+    PI[tid] = yv;
+  } else if (tid < 2 * kST && I != J) {
+    const int cc = tid - kST;
+    PJ[cc] = cadd(colp[0][cc >> 4][cc & 15], colp[1][cc >> 4][cc & 15]);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    last_I = atomicAdd(&cnt[I], 1) == nt - 1;
+    last_J = (I != J) ? atomicAdd(&cnt[J], 1) == nt - 1 : 0;
+    if (last_I) cnt[I] = 0;
+    if (last_J) cnt[J] = 0;
+  }
+  __syncthreads();
+  if (last_I || last_J) __threadfence();
+  for (int pass = 0; pass < 2; ++pass) {
+    const int T = pass == 0 ? I : J;
+    if (!(pass == 0 ? last_I : last_J)) continue;
+    // raw y of row tile T: fixed-order slot sum (four threads per row)
+    {
+      const int row = tid & (kST - 1), qtr = tid >> 6;
+      const int per = (nt + 3) / 4, s_lo = qtr * per, s_hi = min(nt, s_lo + per);
+      const zd* Pr = P + (int64_t)T * nt * kST + row;
+      zd a0 = mk<double>(0, 0), a1 = a0, a2 = a0, a3 = a0;
+      int sl = s_lo;
+      for (; sl + 3 < s_hi; sl += 4) {
+        a0 = cadd(a0, Pr[(int64_t)sl * kST]);
+        a1 = cadd(a1, Pr[(int64_t)(sl + 1) * kST]);
+        a2 = cadd(a2, Pr[(int64_t)(sl + 2) * kST]);
+        a3 = cadd(a3, Pr[(int64_t)(sl + 3) * kST]);
+      }
+      for (; sl < s_hi; ++sl) a0 = cadd(a0, Pr[(int64_t)sl * kST]);
+      quarter[qtr][row] = cadd(cadd(a0, a1), cadd(a2, a3));
+    }
+    __syncthreads();
+    double yr = 0, yi = 0;
+    if (tid < kST) {
+      const int64_t rr = s0 + (int64_t)T * kST + tid;
+      if (rr < n) {
+        const zd yraw = cadd(cadd(quarter[0][tid], quarter[1][tid]), cadd(quarter[2][tid], quarter[3][tid]));
+        y[rr] = yraw;
+        const zd yv = cmulc(yraw, vload(A, n, c, rr, sc));
+        yr = yv.x;
+        yi = yv.y;
+      }
+    }
+    yr = block_sum(yr, red);
+    __syncthreads();
+    yi = block_sum(yi, red);
+    if (tid == 0) {
+      part_yv[(int64_t)T * kPartStride] = yr;
+      part_yv[(int64_t)T * kPartStride + 1] = yi;
+    }
+    __syncthreads();
+  }
+}
+
 // Hermitian completion of the trailing block [s, n)^2 from its lower triangle
 __global__ void k_symmetrize(zd* __restrict__ A, int64_t n, int64_t s0) {
   const int64_t m = n - s0;
@@ -972,7 +1264,7 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
   double* part_p = part + (size_t)kMaxSymvBlk * kPartStride;
   double* part_yv = part + 2 * (size_t)kMaxSymvBlk * kPartStride;
   const int64_t nref = n - 1;
-  int nblk_yv = 0;  // blocks of the previous column's symv (grid path)
+  int nt_prev = 0;  // row tiles of the previous column's matvec (grid path)
   cudaMemsetAsync(tile_cnt, 0, sizeof(int) * (size_t)(ediv(n, kST) + 1), s);
   bool upper_stale = false;  // the grid path keeps only the lower triangle current
   for (int64_t j0 = 0; j0 < nref; j0 += kNB) {
@@ -1007,27 +1299,22 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
       const int nblk_u = (int)ediv(n - c, kRowBlk);
       {
         EigScope sc(ES_TRD_PANEL, s, 16.0 * rows * (2.0 * i + 4.0), 8.0 * rows * (2.0 * i + 3.0));
-        k_trd_upd<<<nblk_u, kRowBlk, 0, s>>>(A, n, VW, j0, i, b, d, tau, y, part_yv, nblk_yv, part_x);
+        k_trd_upd2<<<nblk_u, kRowBlk, 0, s>>>(A, n, VW, j0, i, b, d, tau, y, part_yv, part_p, nt_prev,
+                                              part_x);
         EIG_CHECK();
       }
       if (i >= b) break;
       const int64_t rw = n - c - 1;
-      const int nblk_v = (int)std::max<int64_t>(1, ediv(rw, kRowBlk));
-      {
-        EigScope sc(ES_TRD_PANEL, s, 16.0 * rows * (2.0 * i + 2.0), 8.0 * rows * (2.0 * i + 1.0));
-        k_trd_vec<<<nblk_v, kRowBlk, 0, s>>>(A, n, VW, c, i, e, tau, part_x, nblk_u, part_p);
-        EIG_CHECK();
-      }
       {
         // lower triangle of the trailing block read once: rw (rw + 1) / 2 complex
         const int nt = (int)ediv(rw, kST);
         const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
         EigScope sc(ES_TRD_SYMV, s, 8.0 * (double)rw * (double)(rw + 1) + 16.0 * rw * (2.0 * i + 2.0),
                     8.0 * (double)rw * (double)rw);
-        k_symv_tiles<<<(unsigned)ntiles, 256, 0, s>>>(A, n, c + 1, VW + (int64_t)i * n, nt, slots,
-                                                      tile_cnt, VW, i, part_p, nblk_v, y, part_yv);
+        k_symv_tiles2<<<(unsigned)ntiles, 256, 0, s>>>(A, n, c, VW, i, nt, slots, tile_cnt, part_x, nblk_u,
+                                                       e, tau, y, part_yv, part_p);
         EIG_CHECK();
-        nblk_yv = nt;
+        nt_prev = nt;
       }
     }
     // trailing update A22 -= V W^H + W V^H (rows / cols >= j0 + b): for a full

@@ -114,6 +114,9 @@ def _blob_cases(rng):
     yield "cluster_gram", (u * s) @ w.conj().T
     k = 128
     yield "lowrank_gram", _crandn(rng, 768, k) @ _crandn(rng, k, 1024)
+    # p > 768: the grid-parallel tridiagonalization (fused panel step)
+    k = 400
+    yield "lowrank_grid", _crandn(rng, 1100, k) @ _crandn(rng, k, 1300)
 
 
 @pytest.mark.parametrize("dtype", ["complex128", "complex64"])
@@ -200,7 +203,8 @@ def test_values_only_spectrum(dtype):
     eps = 2e-3
     for name, a in [("lowrank", _crandn(rng, 768, 160) @ _crandn(rng, 160, 640)),
                     ("flat", 0.1 * (_unitary(rng, 600)[:, :300] @ _unitary(rng, 600)[:, :300].conj().T)),
-                    ("graded", (_unitary(rng, 700) * np.logspace(0, -5, 700)) @ _unitary(rng, 700).conj().T)]:
+                    ("graded", (_unitary(rng, 700) * np.logspace(0, -5, 700)) @ _unitary(rng, 700).conj().T),
+                    ("grid", _crandn(rng, 1000, 300) @ _crandn(rng, 300, 1000))]:
         a = a / np.linalg.norm(a)
         if dtype == "complex64":
             a = a.astype(np.complex64).astype(np.complex128)

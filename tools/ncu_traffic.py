@@ -40,14 +40,23 @@ def main():
         if k not in idx:
             raise SystemExit(f"missing column {k}")
     grid_col = next((h for h in hdr if h in ("launch__grid_size", "Grid Size")), None)
+    units = rows[1]
+    scale_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale_t = {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
+    fb_r = scale_b.get(units[idx["dram__bytes_read.sum"]], 1)
+    fb_w = scale_b.get(units[idx["dram__bytes_write.sum"]], 1)
+    ft = scale_t.get(units[idx["gpu__time_duration.sum"]], 1)
     per = defaultdict(list)
     for r in rows[2:]:  # row 1 holds units
         if len(r) < len(hdr):
             continue
         name = r[idx["Kernel Name"]]
-        short = re.sub(r"[<(].*", "", name).strip()
+        short = re.sub(r"[<(].*", "", re.sub(r"^void ", "", name)).strip()
         rd, wr = num(r[idx["dram__bytes_read.sum"]]), num(r[idx["dram__bytes_write.sum"]])
         t = num(r[idx["gpu__time_duration.sum"]])
+        rd = rd * fb_r if rd is not None else None
+        wr = wr * fb_w if wr is not None else None
+        t = t * ft if t is not None else None
         grid = num(r[idx[grid_col]]) if grid_col else None
         if rd is None or wr is None:
             continue
