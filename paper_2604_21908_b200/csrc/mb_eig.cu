@@ -626,12 +626,10 @@ __global__ void __launch_bounds__(256) k_trd_symv(const zd* __restrict__ A, int6
 
 
 // Grid-parallel panel step for large trailing blocks (the single-CTA
-// k_trd_col would serialize O(n * 32) complex work per column on one SM).
-// Three launches per column: k_trd_upd (finish W[:, i-1], update column c,
-// partial |x|^2), k_trd_vec (Householder scalars, reflector, partial V^H v and
-// W^H v), k_symv_tiles (y = A22 v - W p1 - V p2, partial y^H v). All partial
+// k_trd_col would serialize O(n * 32) complex work per column on one SM):
+// k_trd_upd2 + k_symv_tiles2 below, two launches per column. All partial
 // sums are reduced in a fixed order (bitwise reproducible).
-constexpr int kRowBlk = 256;    // rows per block in upd / vec
+constexpr int kRowBlk = 256;    // rows per block in the column update
 constexpr int64_t kGridRows = 768;  // trailing size above which the grid path runs
 constexpr int kMaxSymvBlk = 1184;
 constexpr int kPartStride = 4 * kNB + 4;  // doubles per block partial
@@ -649,140 +647,7 @@ __device__ __forceinline__ zd fixed_sum_cx(const double* part, int nblk, int off
   return mk<double>(re, im);
 }
 
-__global__ void __launch_bounds__(kRowBlk) k_trd_upd(zd* __restrict__ A, int64_t n,
-                                                     zd* __restrict__ VW, int64_t j0, int i, int b,
-                                                     double* __restrict__ dd, const zd* __restrict__ tau,
-                                                     const zd* __restrict__ y,
-                                                     const double* __restrict__ part_yv, int nblk_yv,
-                                                     double* __restrict__ part_x) {
-  __shared__ zd sh_rowv[kNB], sh_roww[kNB];
-  __shared__ zd sh_alpha;
-  __shared__ double red[32];
-  zd* V = VW;
-  zd* W = VW + (int64_t)kNB * n;
-  const int64_t c = j0 + i;          // column to update (if i < b)
-  const int64_t r = c + (int64_t)blockIdx.x * kRowBlk + threadIdx.x;
-  const int t_prev = i - 1;
-  zd tp = mk<double>(0, 0);
-  if (i > 0) {
-    tp = tau[c - 1];
-    if (threadIdx.x < 32) {
-      const zd yv = fixed_sum_cx(part_yv, nblk_yv, 0);
-      if (threadIdx.x == 0) {
-        // alpha = -tau/2 (w^H v), w = tau y  =>  w^H v = conj(tau) (y^H v)
-        const zd whv = cmul(cconj(tp), yv);
-        sh_alpha = cmul(mk<double>(-0.5 * tp.x, -0.5 * tp.y), whv);
-      }
-    }
-    __syncthreads();
-  }
-  const zd al = i > 0 ? sh_alpha : mk<double>(0, 0);
-  zd wr = mk<double>(0, 0);
-  if (i > 0 && r < n) {
-    wr = cadd(cmul(tp, y[r]), cmul(al, V[r + t_prev * n]));
-    W[r + t_prev * n] = wr;
-  }
-  if (i >= b) return;
-  // row c of the panel's V and W (t < i); W[c, i-1] recomputed redundantly
-  if (threadIdx.x < i) {
-    const int t = threadIdx.x;
-    sh_rowv[t] = V[c + t * n];
-    sh_roww[t] = (t == t_prev) ? cadd(cmul(tp, y[c]), cmul(al, V[c + t * n])) : W[c + t * n];
-  }
-  __syncthreads();
-  double xn = 0;
-  if (r < n) {
-    const zd a = panel_row_update(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, t_prev, wr);
-    A[r + c * n] = a;
-    if (r == c) dd[c] = a.x;
-    if (r >= c + 2) xn = cabs2(a);
-  }
-  xn = block_sum(xn, red);
-  if (threadIdx.x == 0) part_x[(int64_t)blockIdx.x * kPartStride] = xn;
-}
 
-__global__ void __launch_bounds__(kRowBlk) k_trd_vec(zd* __restrict__ A, int64_t n,
-                                                     zd* __restrict__ VW, int64_t c, int i,
-                                                     double* __restrict__ ee, zd* __restrict__ tau,
-                                                     const double* __restrict__ part_x, int nblk_x,
-                                                     double* __restrict__ part_p) {
-  __shared__ zd sh_sc;
-  __shared__ zd red_w[kRowBlk / 32][2 * kNB];
-  zd* V = VW;
-  zd* W = VW + (int64_t)kNB * n;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double x = 0;
-    for (int bb = lane; bb < nblk_x; bb += 32) x += part_x[(int64_t)bb * kPartStride];
-    x = warp_sum(x);
-    if (lane == 0) {
-      const zd al = A[(c + 1) + c * n];
-      zd tv, sc;
-      double beta;
-      if (x + al.x * al.x + al.y * al.y < 1e-250) {
-        tv = mk<double>(0, 0);
-        beta = al.x;
-        sc = mk<double>(0, 0);
-      } else {
-        beta = -copysign(sqrt(al.x * al.x + al.y * al.y + x), al.x);
-        tv = mk<double>((beta - al.x) / beta, -al.y / beta);
-        const zd den = mk<double>(al.x - beta, al.y);
-        const double dn = den.x * den.x + den.y * den.y;
-        sc = mk<double>(den.x / dn, -den.y / dn);
-      }
-      sh_sc = sc;
-      if (blockIdx.x == 0) {
-        ee[c] = beta;
-        tau[c] = tv;
-      }
-    }
-  }
-  __syncthreads();
-  const zd sc = sh_sc;
-  const int64_t r = c + 1 + (int64_t)blockIdx.x * kRowBlk + threadIdx.x;
-  zd v = mk<double>(0, 0);
-  if (r < n) {
-    if (r == c + 1) {
-      v = mk<double>(1, 0);
-    } else {
-      v = cmul(A[r + c * n], sc);
-      A[r + c * n] = v;
-    }
-    V[r + i * n] = v;
-  }
-  // partial p1 = V[:, t]^H v, p2 = W[:, t]^H v over this block's rows
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int t0 = 0; t0 < i; t0 += 8) {
-    zd va[8], wa[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      va[u] = mk<double>(0, 0);
-      wa[u] = mk<double>(0, 0);
-      if (r < n && t0 + u < i) {
-        va[u] = cmulc(V[r + (t0 + u) * n], v);
-        wa[u] = cmulc(W[r + (t0 + u) * n], v);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (t0 + u >= i) break;
-      const double ar = warp_sum(va[u].x), ai = warp_sum(va[u].y);
-      const double wr = warp_sum(wa[u].x), wi = warp_sum(wa[u].y);
-      if (lane == 0) {
-        red_w[wid][t0 + u] = mk<double>(ar, ai);
-        red_w[wid][kNB + t0 + u] = mk<double>(wr, wi);
-      }
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
-    const int t = e < i ? e : kNB + (e - i);
-    zd acc = mk<double>(0, 0);
-    for (int w2 = 0; w2 < kRowBlk / 32; ++w2) acc = cadd(acc, red_w[w2][t]);
-    part_p[(int64_t)blockIdx.x * kPartStride + 2 * t] = acc.x;
-    part_p[(int64_t)blockIdx.x * kPartStride + 2 * t + 1] = acc.y;
-  }
-}
 
 
 // dst[r, t] = src[r, t] for r < m, t < b (column-major, leading dimension ld)
@@ -799,152 +664,11 @@ __global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, in
 // HBM traffic of a full-column sweep): the trailing block [s, n)^2 is tiled
 // 64 x 64; a lower tile (I, J), I > J, contributes A_IJ v_J to y_I and
 // A_IJ^H v_I to y_J, a diagonal tile its Hermitian completion to y_I. Each
-// contribution lands in its own slot P[row tile][other tile] (no atomics);
-// the row tile's last contributor adds the slots in a fixed order.
+// contribution lands in its own slot P[row tile][other tile]; the block that
+// completes a row tile (last of its nt contributions, counted with an atomic
+// per tile) reduces that tile's slots in a fixed order (k_symv_tiles2).
 constexpr int kST = 64;
 
-// The block that completes a row tile (last of its nt contributions, counted
-// with an atomic per tile) also reduces that tile's slots in a fixed order,
-// applies the panel corrections and writes y and the tile's y^H v partial —
-// no separate reduction launch.
-__device__ void symv_finish_tile(const zd* __restrict__ P, int nt, int64_t n, int64_t s0, int I,
-                                 const zd* __restrict__ VW, int i, const double* __restrict__ part_p,
-                                 int nblk_p, zd* __restrict__ y, double* __restrict__ part_yv,
-                                 zd* pv, double* red) {
-  const zd* V = VW;
-  const zd* W = VW + (int64_t)kNB * n;
-  for (int e = threadIdx.x; e < 2 * i; e += blockDim.x) {
-    const int t = e < i ? e : kNB + (e - i);
-    double re = 0, im = 0;
-    for (int bb = 0; bb < nblk_p; ++bb) {
-      re += part_p[(int64_t)bb * kPartStride + 2 * t];
-      im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
-    }
-    pv[t] = mk<double>(re, im);
-  }
-  __syncthreads();
-  const zd* v = V + (int64_t)i * n;
-  // slot sums: four threads per row, each a contiguous quarter of the slots
-  // with four loads in flight, combined in a fixed order
-  __shared__ zd quarter[4][kST];
-  {
-    const int row = threadIdx.x & (kST - 1), qtr = threadIdx.x >> 6;
-    const int per = (nt + 3) / 4, s_lo = qtr * per, s_hi = min(nt, s_lo + per);
-    const zd* Pr = P + (int64_t)I * nt * kST + row;
-    zd a0 = mk<double>(0, 0), a1 = a0, a2 = a0, a3 = a0;
-    int sl = s_lo;
-    for (; sl + 3 < s_hi; sl += 4) {
-      a0 = cadd(a0, Pr[(int64_t)sl * kST]);
-      a1 = cadd(a1, Pr[(int64_t)(sl + 1) * kST]);
-      a2 = cadd(a2, Pr[(int64_t)(sl + 2) * kST]);
-      a3 = cadd(a3, Pr[(int64_t)(sl + 3) * kST]);
-    }
-    for (; sl < s_hi; ++sl) a0 = cadd(a0, Pr[(int64_t)sl * kST]);
-    quarter[qtr][row] = cadd(cadd(a0, a1), cadd(a2, a3));
-  }
-  __syncthreads();
-  double yr = 0, yi = 0;
-  if (threadIdx.x < kST) {
-    const int64_t r = s0 + (int64_t)I * kST + threadIdx.x;
-    if (r < n) {
-      zd acc = cadd(cadd(quarter[0][threadIdx.x], quarter[1][threadIdx.x]),
-                    cadd(quarter[2][threadIdx.x], quarter[3][threadIdx.x]));
-      for (int t = 0; t < i; ++t) {
-        acc = csub(acc, cmul(W[r + t * n], pv[t]));
-        acc = csub(acc, cmul(V[r + t * n], pv[kNB + t]));
-      }
-      y[r] = acc;
-      const zd yv = cmulc(acc, v[r]);
-      yr = yv.x;
-      yi = yv.y;
-    }
-  }
-  yr = block_sum(yr, red);
-  __syncthreads();
-  yi = block_sum(yi, red);
-  if (threadIdx.x == 0) {
-    part_yv[(int64_t)I * kPartStride] = yr;
-    part_yv[(int64_t)I * kPartStride + 1] = yi;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_symv_tiles(const zd* __restrict__ A, int64_t n, int64_t s0,
-                                                    const zd* __restrict__ v, int nt,
-                                                    zd* __restrict__ P, int* __restrict__ cnt,
-                                                    const zd* __restrict__ VW, int i,
-                                                    const double* __restrict__ part_p, int nblk_p,
-                                                    zd* __restrict__ y, double* __restrict__ part_yv) {
-  __shared__ zd vI[kST], vJ[kST];
-  __shared__ zd rowp[4][kST];
-  __shared__ zd colp[2][4][16];
-  __shared__ zd pv[2 * kNB];
-  __shared__ double red[32];
-  __shared__ int last_I, last_J;
-  // lower-tile index -> (I, J), I >= J
-  const int64_t t = blockIdx.x;
-  int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(I + 1) * (I + 2) / 2 <= t) ++I;
-  while ((int64_t)I * (I + 1) / 2 > t) --I;
-  const int J = (int)(t - (int64_t)I * (I + 1) / 2);
-  const int tid = threadIdx.x, tr = tid & 63, tg = tid >> 6;
-  const int64_t r0 = s0 + (int64_t)I * kST, c0 = s0 + (int64_t)J * kST;
-  if (tid < kST) {
-    vI[tid] = r0 + tid < n ? v[r0 + tid] : mk<double>(0, 0);
-    vJ[tid] = c0 + tid < n ? v[c0 + tid] : mk<double>(0, 0);
-  }
-  __syncthreads();
-  const int64_t r = r0 + tr;
-  zd a[16];
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int cc = tg * 16 + u;
-    const int64_t c = c0 + cc;
-    a[u] = (r < n && c < n && (I != J || tr >= cc)) ? A[r + c * n] : mk<double>(0, 0);
-  }
-  zd acc = mk<double>(0, 0);
-#pragma unroll
-  for (int u = 0; u < 16; ++u) acc = cadd(acc, cmul(a[u], vJ[tg * 16 + u]));
-  rowp[tg][tr] = acc;
-  // column part: conj(A_rc) v_r summed over the tile's rows (strictly lower)
-  const int lane = tid & 31, half = (tid >> 5) & 1;
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int cc = tg * 16 + u;
-    zd x = (I != J || tr > cc) ? cmulc(a[u], vI[tr]) : mk<double>(0, 0);
-    x.x = warp_sum(x.x);
-    x.y = warp_sum(x.y);
-    if (lane == 0) colp[half][tg][u] = x;
-  }
-  __syncthreads();
-  zd* PI = P + ((int64_t)I * nt + J) * kST;  // slot of (I, J) in row tile I
-  zd* PJ = P + ((int64_t)J * nt + I) * kST;  // slot of (I, J) in row tile J
-  if (tid < kST) {
-    zd y = cadd(cadd(rowp[0][tid], rowp[1][tid]), cadd(rowp[2][tid], rowp[3][tid]));
-    if (I == J) {
-      // diagonal tile: the strictly-lower part's transpose contribution
-      const zd cpart = cadd(colp[0][tid >> 4][tid & 15], colp[1][tid >> 4][tid & 15]);
-      y = cadd(y, cpart);
-    }
-    PI[tid] = y;
-  } else if (tid < 2 * kST && I != J) {
-    const int cc = tid - kST;
-    PJ[cc] = cadd(colp[0][cc >> 4][cc & 15], colp[1][cc >> 4][cc & 15]);
-  }
-  // completion counting: this tile feeds row tile I (and J when I != J)
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    last_I = atomicAdd(&cnt[I], 1) == nt - 1;
-    last_J = (I != J) ? atomicAdd(&cnt[J], 1) == nt - 1 : 0;
-    if (last_I) cnt[I] = 0;  // reset for the next launch
-    if (last_J) cnt[J] = 0;
-  }
-  __syncthreads();
-  if (last_I || last_J) __threadfence();
-  if (last_I) symv_finish_tile(P, nt, n, s0, I, VW, i, part_p, nblk_p, y, part_yv, pv, red);
-  __syncthreads();
-  if (last_J) symv_finish_tile(P, nt, n, s0, J, VW, i, part_p, nblk_p, y, part_yv, pv, red);
-}
 
 // ---- fused panel step (grid path): two launches per column --------------------
 //
