@@ -407,6 +407,8 @@ def main():
 
     prefix = _prefix(args)
 
+    last_result = []
+
     def one_step():
         job = Contraction(inst.circuit, cfg, comm)
         if prefix:
@@ -414,6 +416,7 @@ def main():
             return job, None
         job.advance()
         res = job.finish()
+        last_result[:] = [res]
         return job, peak_output(res)
 
     def warm_step():
@@ -496,6 +499,15 @@ def main():
     h2d = (c1["h2d_bytes"] - c0["h2d_bytes"]) // args.steps + len(qasm)
     d2h = (c1["d2h_bytes"] - c0["d2h_bytes"]) // args.steps
 
+    sampled_top = None
+    if last_result:
+        # the greedy sweep's answer against the reference's method: the top
+        # count of 1000 exact samples (untimed)
+        from collections import Counter
+
+        from paper_2604_21908_b200.driver import sample_output
+
+        sampled_top = Counter(sample_output(last_result[0], 1000, seed=0)).most_common(1)[0][0]
     if rank == 0:
         hbm, bf16, src = _peaks()
         roof = _roofline(prof, stages, hbm, src, fp64, dev_ms)
@@ -521,6 +533,8 @@ def main():
                            source_gates_per_step=gates_step),
             "peak": ({"bits": peaks[-1][0], "probability": peaks[-1][1],
                       "planted": inst.peak, "match": peaks[-1][0] == inst.peak,
+                      "sampled_top_1000": sampled_top,
+                      "greedy_equals_sampled_top": sampled_top == peaks[-1][0],
                       "e2e_bits_match": bits == peaks[-1][0]} if peaks[-1] is not None else
                      {"bits": None, "note": f"timed step = first {prefix} absorption steps; the full "
                       "contraction of this instance is reported in profiles/r02_c56_full.jsonl"}),

@@ -251,7 +251,14 @@ def sample(psi: MatrixProductState, shots: int, seed: int) -> list[str]:
 def extract_peak(psi: MatrixProductState) -> tuple[str, float]:
     """Greedy sequential marginal sweep on the device: at each site keep the
     more probable branch given the chosen prefix. Returns the bitstring
-    (qubit 0 leftmost) and its exact probability |<x|psi>|^2."""
+    (qubit 0 leftmost) and its exact probability |<x|psi>|^2.
+
+    This is a *greedy* peak: it is guaranteed to be the argmax only when the
+    peak carries more than half the weight (each conditional then exceeds
+    1/2). For peaked circuits with a 10% planted peak it can in principle
+    differ from the reference's answer, the top count of samples
+    (cli.py:167-173); callers that report a match cross-check it against
+    sampled counts (bench.py does)."""
     n = psi.num_sites
     bits = np.empty(n, dtype=np.uint8)
     probs = np.empty(n, dtype=np.float64)

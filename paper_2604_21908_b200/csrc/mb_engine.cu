@@ -526,9 +526,8 @@ static void dump_matrix(const char* tag, const cx<R>* dev, int64_t m, int64_t n,
   }
 }
 
-// Center moves through the explicit-Q Householder kernels (2p launches) are
-// opt-in (MB_QR_STEPS=1); by default they use the SVD split (same shapes).
-// Left-orthogonalize site i, pushing the remainder into site i+1 (chains.py:110).
+// Center moves use the untruncated SVD split (the reduced QR's shapes; only
+// the gauge differs). Left-orthogonalize site i, pushing the remainder into site i+1 (chains.py:110).
 template <typename R>
 static void push_right(mb_chain& c, int i) {
   const int d = c.d;
