@@ -424,14 +424,15 @@ constexpr int kMaxSplit = 8;   // split-K slices
 // a -= sum_{t<i} V[r,t] conj(rw[t]) + W[r,t] conj(rv[t]); W[r, t_over] is
 // replaced by w_over. Loads are issued eight at a time (independent), so a
 // row costs a few memory latencies instead of 2 i dependent ones.
+template <int NBATCH>
 __device__ __forceinline__ zd panel_row_update(zd a, const zd* __restrict__ V,
                                                const zd* __restrict__ W, int64_t r, int64_t n,
                                                int i, const zd* rv, const zd* rw, int t_over,
                                                zd w_over) {
-  for (int t0 = 0; t0 < i; t0 += 8) {
-    zd vv[8], ww[8];
+  for (int t0 = 0; t0 < i; t0 += NBATCH) {
+    zd vv[NBATCH], ww[NBATCH];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < NBATCH; ++u) {
       const int t = t0 + u;
       if (t < i) {
         vv[u] = V[r + t * n];
@@ -439,7 +440,7 @@ __device__ __forceinline__ zd panel_row_update(zd a, const zd* __restrict__ V,
       }
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < NBATCH; ++u) {
       const int t = t0 + u;
       if (t < i) {
         a = csub(a, cmul(vv[u], cconj(rw[t])));
@@ -484,7 +485,7 @@ __device__ __forceinline__ zd col_dot(const zd* __restrict__ col, const zd* __re
 //   w = tau y; alpha = -tau/2 (w^H v); w += alpha v.
 // Part B (i < b): column c = j0 + i: apply the panel's earlier reflectors,
 // d[c], Householder vector (zlarfg), p1 / p2 for the next symv.
-__global__ void __launch_bounds__(1024) k_trd_col(zd* __restrict__ A, int64_t n, zd* __restrict__ VW,
+__global__ void __launch_bounds__(512) k_trd_col(zd* __restrict__ A, int64_t n, zd* __restrict__ VW,
                                                   int64_t j0, int i, int b, double* __restrict__ dd,
                                                   double* __restrict__ ee, zd* __restrict__ tau,
                                                   zd* __restrict__ pv, const zd* __restrict__ y) {
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(1024) k_trd_col(zd* __restrict__ A, int64_t n,
   // column update: A[r, c] -= sum_t V[r,t] conj(W[c,t]) + W[r,t] conj(V[c,t])
   double xn = 0;
   for (int64_t r = c + tid; r < n; r += nt) {
-    const zd a = panel_row_update(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, -1,
+    const zd a = panel_row_update<8>(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, -1,
                                   mk<double>(0, 0));
     A[r + c * n] = a;
     if (r >= c + 2) xn += cabs2(a);
@@ -683,16 +684,16 @@ constexpr int kST = 64;
 // y_r - sum_{t < nt_} (W[r,t] p1[t] + V[r,t] p2[t]) with batched loads
 __device__ __forceinline__ zd row_corrected(zd yr, const zd* __restrict__ V, const zd* __restrict__ W,
                                            int64_t r, int64_t n, int nt_, const zd* pv) {
-  for (int t0 = 0; t0 < nt_; t0 += 8) {
-    zd vv[8], ww[8];
+  for (int t0 = 0; t0 < nt_; t0 += 16) {
+    zd vv[16], ww[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 16; ++u)
       if (t0 + u < nt_) {
         vv[u] = V[r + (t0 + u) * n];
         ww[u] = W[r + (t0 + u) * n];
       }
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 16; ++u)
       if (t0 + u < nt_) {
         yr = csub(yr, cmul(ww[u], pv[t0 + u]));
         yr = csub(yr, cmul(vv[u], pv[kNB + t0 + u]));
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(kRowBlk) k_trd_upd2(zd* __restrict__ A, int64_
   __syncthreads();
   double xn = 0;
   if (r < n) {
-    const zd a = panel_row_update(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, tp_i, wr);
+    const zd a = panel_row_update<16>(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, tp_i, wr);
     A[r + c * n] = a;
     if (r == c) dd[c] = a.x;
     if (r >= c + 2) xn = cabs2(a);
