@@ -669,6 +669,7 @@ __global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, in
 // completes a row tile (last of its nt contributions, counted with an atomic
 // per tile) reduces that tile's slots in a fixed order (k_symv_tiles2).
 constexpr int kST = 64;
+constexpr int kTileSmem = kST * (kST + 1) * 16;  // one complex128 tile, padded rows
 
 
 // ---- fused panel step (grid path): two launches per column --------------------
@@ -791,9 +792,10 @@ __global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, i
                                                      double* __restrict__ ee, zd* __restrict__ tau,
                                                      zd* __restrict__ y, double* __restrict__ part_yv,
                                                      double* __restrict__ part_p) {
+  extern __shared__ zd tile[];  // kST x (kST + 1)
   __shared__ zd vI[kST], vJ[kST];
   __shared__ zd rowp[4][kST];
-  __shared__ zd colp[2][4][16];
+  __shared__ zd colq[4][kST];
   __shared__ zd quarter[4][kST];
   __shared__ zd sh_sc;
   __shared__ zd red_w[2][2 * kNB];
@@ -844,27 +846,33 @@ __global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, i
     vJ[tid] = vload(A, n, c, c0 + tid, sc);
   }
   __syncthreads();
+  // the 64 x 64 tile staged in shared memory (16 independent loads per
+  // thread), then row sums (four threads per row) and column sums (four
+  // threads per column) straight from shared memory — no shuffle chains
   const int64_t r = r0 + tr;
-  zd a[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int cc = tg * 16 + u;
     const int64_t cg = c0 + cc;
-    a[u] = (r < n && cg < n && (I != J || tr >= cc)) ? A[r + cg * n] : mk<double>(0, 0);
+    tile[tr * (kST + 1) + cc] =
+        (r < n && cg < n && (I != J || tr >= cc)) ? A[r + cg * n] : mk<double>(0, 0);
   }
-  zd acc = mk<double>(0, 0);
+  __syncthreads();
+  {
+    zd acc = mk<double>(0, 0);
 #pragma unroll
-  for (int u = 0; u < 16; ++u) acc = cadd(acc, cmul(a[u], vJ[tg * 16 + u]));
-  rowp[tg][tr] = acc;
-  const int lane = tid & 31, half = (tid >> 5) & 1;
+    for (int u = 0; u < 16; ++u) acc = cadd(acc, cmul(tile[tr * (kST + 1) + tg * 16 + u], vJ[tg * 16 + u]));
+    rowp[tg][tr] = acc;
+    // column cc = tr over rows tg*16 .. tg*16+15 (strictly lower on the diagonal)
+    zd cacc = mk<double>(0, 0);
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int cc = tg * 16 + u;
-    zd x = (I != J || tr > cc) ? cmulc(a[u], vI[tr]) : mk<double>(0, 0);
-    x.x = warp_sum(x.x);
-    x.y = warp_sum(x.y);
-    if (lane == 0) colp[half][tg][u] = x;
+    for (int u = 0; u < 16; ++u) {
+      const int rr = tg * 16 + u;
+      if (I != J || rr > tr) cacc = cadd(cacc, cmulc(tile[rr * (kST + 1) + tr], vI[rr]));
+    }
+    colq[tg][tr] = cacc;
   }
+  const int lane = tid & 31;
   // diagonal tiles publish v and the partial V^H v, W^H v of their rows
   if (I == J && tid < kST) {
     const int64_t rr = r0 + tid;
@@ -905,11 +913,11 @@ __global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, i
   zd* PJ = P + ((int64_t)J * nt + I) * kST;
   if (tid < kST) {
     zd yv = cadd(cadd(rowp[0][tid], rowp[1][tid]), cadd(rowp[2][tid], rowp[3][tid]));
-    if (I == J) yv = cadd(yv, cadd(colp[0][tid >> 4][tid & 15], colp[1][tid >> 4][tid & 15]));
+    if (I == J) yv = cadd(yv, cadd(cadd(colq[0][tid], colq[1][tid]), cadd(colq[2][tid], colq[3][tid])));
     PI[tid] = yv;
   } else if (tid < 2 * kST && I != J) {
     const int cc = tid - kST;
-    PJ[cc] = cadd(colp[0][cc >> 4][cc & 15], colp[1][cc >> 4][cc & 15]);
+    PJ[cc] = cadd(cadd(colq[0][cc], colq[1][cc]), cadd(colq[2][cc], colq[3][cc]));
   }
   __threadfence();
   __syncthreads();
@@ -1036,8 +1044,8 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
         const int64_t ntiles = (int64_t)nt * (nt + 1) / 2;
         EigScope sc(ES_TRD_SYMV, s, 8.0 * (double)rw * (double)(rw + 1) + 16.0 * rw * (2.0 * i + 2.0),
                     8.0 * (double)rw * (double)rw);
-        k_symv_tiles2<<<(unsigned)ntiles, 256, 0, s>>>(A, n, c, VW, i, nt, slots, tile_cnt, part_x, nblk_u,
-                                                       e, tau, y, part_yv, part_p);
+        k_symv_tiles2<<<(unsigned)ntiles, 256, kTileSmem, s>>>(A, n, c, VW, i, nt, slots, tile_cnt, part_x,
+                                                               nblk_u, e, tau, y, part_yv, part_p);
         EIG_CHECK();
         nt_prev = nt;
       }
@@ -1096,6 +1104,10 @@ static const bool kTrdGraphs = !getenv("MB_TRD_GRAPH") || atoi(getenv("MB_TRD_GR
 static void hetrd_replay(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* pv, zd* y,
                          double* part, zd* slots, int* tile_cnt, const void* base,
                          cudaStream_t s) {
+  static const bool attr = (cudaFuncSetAttribute(k_symv_tiles2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kTileSmem),
+                            true);
+  (void)attr;
   TrdGraphCache& C = g_trd_graphs;
   ++C.tick;
   if (kTrdGraphs && n >= 128) {
