@@ -1110,7 +1110,10 @@ static void hetrd_replay(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau
   (void)attr;
   TrdGraphCache& C = g_trd_graphs;
   ++C.tick;
-  if (kTrdGraphs && n >= 128) {
+  // graphs pay off where the per-column launch chain dominates; above ~2k
+  // columns the kernels' own work hides the launches and a capture (tens of
+  // thousands of nodes) would cost more than it saves
+  if (kTrdGraphs && n >= 128 && n <= 2048) {
     for (auto& en : C.graphs)
       if (en.n == n && en.base == base) {
         en.last = C.tick;
