@@ -88,6 +88,14 @@ def _instance(name):
     return generate(n, depth, w, obf, _SEED.get(name, seed), hidden_permutation=hidden)
 
 
+def _config(args, prefix, dtype="complex128"):
+    """The workload both arms time (identical dicts in the two lines)."""
+    return dict(_workload(args.config, dtype),
+                step=(f"first {prefix} absorption steps of the contraction (fixed prefix, same "
+                      "circuit and settings in both arms)" if prefix else
+                      "full contraction + peak extraction"))
+
+
 def _workload(name, dtype):
     n, depth, w, obf, seed, hidden = CONFIGS[name]
     seed = _SEED.get(name, seed)
@@ -253,7 +261,9 @@ def run_reference(args, rank, world):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic (reference generator, seeded)",
-            "config": _workload(args.config, "complex128"),
+            "config": _config(args, steps if _prefix(args) else 0),
+            "arm": {"parallelism": f"{timed[-1]['threads']} host threads (numpy/OpenBLAS)",
+                    "source_gates_per_step": [r["source_gates"] for r in timed]},
             "cpu_baseline": {"value": val, "unit": "source 2q gates absorbed/s",
                              "cores": timed[-1]["threads"], "kind": "port",
                              "sample": _sample_text(args.config, timed[-1])},
@@ -520,17 +530,14 @@ def main():
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "c128" if args.dtype == "complex128" else "c64",
             "data": "synthetic (reference generator, seeded)",
-            "config": dict(_workload(args.config, args.dtype),
-                           parallelism=(f"sharded unswap scoring x{world} (NCCL all-reduce)"
-                                        if world > 1 else "1 GPU"),
-                           unswap_order="parity-batched" if world > 1 else "parity-parallel",
-                           warmup_steps=(f"first {args.warm_prefix} absorption steps" if big and args.warm_prefix
-                                         else "full contractions"),
-                           timed_region="per-class / per-stage CUDA events on (roofline durations)",
-                           step=(f"first {prefix} absorption steps of the contraction (fixed prefix, "
-                                 "same circuit and settings)" if prefix else
-                                 "full contraction + peak extraction"),
-                           source_gates_per_step=gates_step),
+            "config": _config(args, prefix, args.dtype),
+            "arm": {"parallelism": (f"sharded unswap scoring x{world} (NCCL all-reduce)"
+                                    if world > 1 else "1 GPU"),
+                    "unswap_order": "parity-batched" if world > 1 else "parity-parallel",
+                    "warmup_steps": (f"first {args.warm_prefix} absorption steps" if big and args.warm_prefix
+                                     else "full contractions"),
+                    "timed_region": "per-class / per-stage CUDA events on (roofline durations)",
+                    "source_gates_per_step": gates_step},
             "peak": ({"bits": peaks[-1][0], "probability": peaks[-1][1],
                       "planted": inst.peak, "match": peaks[-1][0] == inst.peak,
                       "sampled_top_1000": sampled_top,
