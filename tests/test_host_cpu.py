@@ -237,3 +237,28 @@ def test_hs_overlap_transfer_sweep_matches_dense():
     assert np.isclose(np.exp(lg) * ph, ref, rtol=1e-12)
     la, _ = hs_overlap(a, a)
     assert np.isclose(np.exp(la), np.vdot(dense(a), dense(a)).real, rtol=1e-12)
+
+
+def test_bench_arms_time_the_same_workload():
+    """bench.py: the B200 arm and the reference arm describe the same
+    workload (identical config dicts), and on configs[2]/[3] both time the
+    same fixed absorption prefix."""
+    import argparse
+    import bench
+
+    for name in ("c56", "c36"):
+        args = argparse.Namespace(config=name, prefix_steps=None, dtype="complex128")
+        pre = bench._prefix(args)
+        assert pre == bench.DEFAULT_PREFIX
+        assert bench._config(args, pre, "complex128") == bench._config(args, pre)
+        assert "first 128 absorption steps" in bench._config(args, pre)["step"]
+    args = argparse.Namespace(config="c20", prefix_steps=None, dtype="complex128")
+    assert bench._prefix(args) == 0
+
+
+def test_svd_convergence_error_is_the_reference_exception_name():
+    from paper_2604_21908_b200 import tensor
+    from paper_2604_21908_b200._native import NativeError
+
+    assert issubclass(tensor.SvdConvergenceError, RuntimeError)
+    assert issubclass(tensor.SvdConvergenceError, NativeError)
