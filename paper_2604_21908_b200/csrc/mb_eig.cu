@@ -999,7 +999,9 @@ static void hetrd(zd* A, int64_t n, zd* VW, double* d, double* e, zd* tau, zd* p
   const int64_t nref = n - 1;
   int nt_prev = 0;  // row tiles of the previous column's matvec (grid path)
   cudaMemsetAsync(tile_cnt, 0, sizeof(int) * (size_t)(ediv(n, kST) + 1), s);
-  bool upper_stale = false;  // the grid path keeps only the lower triangle current
+  // the input (the Gram) holds its lower triangle only, and the grid path
+  // keeps only the lower triangle current
+  bool upper_stale = true;
   for (int64_t j0 = 0; j0 < nref; j0 += kNB) {
     const int b = (int)std::min<int64_t>(kNB, nref - j0);
     // one CTA per panel step while the trailing block is small; the grid
@@ -2131,7 +2133,7 @@ __global__ void k_gram_offdiag(const zd* __restrict__ G, int64_t p, double tol, 
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p * p;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e % p, c = e / p;
-    if (r >= c) continue;
+    if (r <= c) continue;  // the Gram is formed on its lower triangle
     const zd g = G[e];
     const double a = sqrt(g.x * g.x + g.y * g.y);
     const double gr = G[r + r * p].x, gc = G[c + c * p].x;
@@ -2167,7 +2169,7 @@ void svd_gram(SvdJob<R>& J, void* ws, cudaStream_t s) {
     EIG_CHECK();
   }
   // 1. G = X^H X in fp64
-  gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s);
+  gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s, true);
   {
     // already orthogonal columns: V = I, sigma = column norms (one read-back)
     static thread_local int* h_flag = nullptr;
@@ -2272,7 +2274,7 @@ void gram_precondition(SvdJob<R>& J, void* ws, cudaStream_t s) {
   char* B = base_ptr(ws);
   zd* G = (zd*)(B + off[L_G]);
   zd* Vc = (zd*)(B + off[L_QS]);
-  gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s);
+  gemm_cm<cx<R>, zd, true, false>(ES_GRAM, p, p, q, 1.0, J.X, q, J.X, q, 0.0, G, p, s, true);
   heevd(p, ws, s, nullptr);
   cx<R>* VG = reinterpret_cast<cx<R>*>(J.W + q * p);
   {
