@@ -183,10 +183,10 @@ int mb_svd_truncate(const double* a, int64_t m, int64_t n, int dtype, double eps
  * The Gram eigenproblem behind the truncated SVD of tensor.py:84-116. */
 int mb_herm_eig(const double* a, int64_t n, double* w, double* v);
 /* Test hook: the next n convergence outcomes of the large Jacobi path count
- * as failures. A failure is retried twice (restart from the Gram
- * eigenvectors, then the reference's perturbed copy); a third makes the call
- * fail with MB_ERR_NUMERIC (SvdConvergenceError in Python), the contract of
- * _svd_with_retry (tensor.py:139-150). */
+ * as failures. A failed factorization is retried (further passes, a restart
+ * from the Gram eigenvectors, then the reference's perturbed copy); when every
+ * attempt fails the call returns MB_ERR_NUMERIC (SvdConvergenceError in
+ * Python), the contract of _svd_with_retry (tensor.py:139-150). */
 int mb_debug_fail_svd(int n);
 
 #ifdef __cplusplus

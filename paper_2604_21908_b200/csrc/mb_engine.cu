@@ -283,6 +283,10 @@ static void gemm(bool ct, int64_t M, int64_t N, int64_t K, const cx<R>* A, int64
 // exact (untruncated) large splits at or above this width start from the
 // Gram eigenvectors instead of the identity (MB_SEED_JACOBI_P, 0 = never)
 static const int64_t kSeedJacobiP = getenv("MB_SEED_JACOBI_P") ? atoll(getenv("MB_SEED_JACOBI_P")) : 1024;
+// large jobs up to this width first get kTryPasses plain Jacobi passes
+// (MB_TRY_JACOBI_P, 0 = never)
+static const int64_t kTryJacobiP = getenv("MB_TRY_JACOBI_P") ? atoll(getenv("MB_TRY_JACOBI_P")) : 2048;
+static const int kTryPasses = 3;
 
 template <typename R>
 static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double eps, int64_t chi,
@@ -373,58 +377,65 @@ static void run_jobs(SvdJob<R>* jobs, int nj) {
       dump_matrix<R>("large", jobs[i].A, jobs[i].m, jobs[i].n, seq);
     const bool gram = gram_path_ok(p, jobs[i].eps);
     const double q = (double)(jobs[i].m < jobs[i].n ? jobs[i].n : jobs[i].m), pd = (double)p;
-    if (gram) {
-      // truncated / values-only: fp64 Gram eigenproblem (mb_eig.cu)
-      ProfScope ps(P_SVD_LARGE, 8.0 * q * pd * pd * 2.0 + (16.0 / 3.0 + 8.0 + 2.0) * pd * pd * pd);
-      void* ws = grow(E.eigws, eig_workspace_bytes(p));
+    // Jacobi scratch (host-driven passes)
+    double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
+    const int64_t cap = large_pair_capacity(p);
+    if (E.h_lg_cap < cap) {
+      if (E.h_lg) {
+        ck(cudaStreamSynchronize(E.stream), "sync");
+        cudaFreeHost(E.h_lg);
+      }
+      ck(cudaMallocHost(&E.h_lg, sizeof(int) * 3 * cap), "pinned");
+      E.h_lg_cap = cap;
+    }
+    int* lg = (int*)grow(E.lg_dev, sizeof(int) * 3 * cap);
+    LargeScratch lws{reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, lg, E.h_lg, lg + cap,
+                     E.h_lg + cap};
+    auto ensure_w = [&]() {
       if (!jobs[i].W)  // values-only batch jobs: Y and V in shared scratch
         jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
                                  large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
+    };
+    // up to kTryJacobiP columns, a few Jacobi passes first: blobs that are
+    // already nearly orthogonal (most canonical-form splits) finish there
+    int sweeps = 0;
+    bool conv = false, tried = false;
+    if (p <= kTryJacobiP && jobs[i].A) {
+      ProfScope ps(P_SVD_JACOBI, 2.0 * 8.0 * pd * pd * q);
+      conv = jacobi_large<R>(jobs[i], lws, E.stream, true, false, sweeps, kTryPasses);
+      tried = true;
+    }
+    if (conv) {
+      finish_large<R>(jobs[i], 1, sweeps, E.stream);
+    } else if (gram) {
+      // truncated / values-only: fp64 Gram eigenproblem (mb_eig.cu), from J.A
+      ProfScope ps(P_SVD_LARGE, 8.0 * q * pd * pd * 2.0 + (16.0 / 3.0 + 8.0 + 2.0) * pd * pd * pd);
+      void* ws = grow(E.eigws, eig_workspace_bytes(p));
+      ensure_w();
       svd_gram<R>(jobs[i], ws, E.stream);
       finish_large<R>(jobs[i], 1, 0, E.stream);
     } else {
-      // exact splits and tight cutoffs: block one-sided Jacobi
+      // exact splits and tight cutoffs: block one-sided Jacobi; when the quick
+      // passes (or, above kTryJacobiP, a direct start) do not converge, the
+      // sweeps restart from the Gram eigenvectors, then the reference's
+      // perturbed retry
       ProfScope ps(P_SVD_JACOBI, 2.0 * 8.0 * pd * pd * q);
-      double* scr = (double*)grow(E.d_partial, 512 * sizeof(double));
-      const int64_t cap = large_pair_capacity(p);
-      if (E.h_lg_cap < cap) {
-        if (E.h_lg) {
-          ck(cudaStreamSynchronize(E.stream), "sync");
-          cudaFreeHost(E.h_lg);
+      if (!tried) {
+        if (p >= kSeedJacobiP && jobs[i].A) {
+          init_large<R>(jobs[i], lws, E.stream);
+        } else {
+          conv = jacobi_large<R>(jobs[i], lws, E.stream, true, false, sweeps);
         }
-        ck(cudaMallocHost(&E.h_lg, sizeof(int) * 3 * cap), "pinned");
-        E.h_lg_cap = cap;
+      } else if (p < kSeedJacobiP) {
+        conv = jacobi_large<R>(jobs[i], lws, E.stream, false, false, sweeps);  // more passes
       }
-      int* lg = (int*)grow(E.lg_dev, sizeof(int) * 3 * cap);
-      LargeScratch ws{reinterpret_cast<int*>(E.d_flag->p), E.h_flag, scr, lg, E.h_lg, lg + cap,
-                      E.h_lg + cap};
-      // block Jacobi; on non-convergence: Gram-preconditioned restart (direct
-      // eigensolver seeds the sweeps), then the reference's perturbed retry
-      int sweeps = 0;
-      bool conv;
-      bool seeded = false;
-      if (p >= kSeedJacobiP && jobs[i].A) {
-        // big exact splits: seed the sweeps with the Gram eigenvectors first
-        // (plain block Jacobi needs tens of passes on these blobs)
-        if (!jobs[i].W)
-          jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
-                                   large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
-        init_large<R>(jobs[i], ws, E.stream);
+      if (!conv) {
+        ensure_w();
         gram_precondition<R>(jobs[i], grow(E.eigws, eig_workspace_bytes(p)), E.stream);
-        conv = jacobi_large<R>(jobs[i], ws, E.stream, false, false, sweeps);
-        seeded = true;
-      } else {
-        conv = jacobi_large<R>(jobs[i], ws, E.stream, true, false, sweeps);
-      }
-      if (!conv && !seeded) {
-        if (!jobs[i].W)
-          jobs[i].W = (cx<R>*)grow(E.W[Engine::kSlots - 1],
-                                   large_workspace_elems<R>(jobs[i].m, jobs[i].n) * sizeof(cx<R>));
-        gram_precondition<R>(jobs[i], grow(E.eigws, eig_workspace_bytes(p)), E.stream);
-        conv = jacobi_large<R>(jobs[i], ws, E.stream, false, false, sweeps);
+        conv = jacobi_large<R>(jobs[i], lws, E.stream, false, false, sweeps);
         E.counters[3]++;
       }
-      if (!conv) conv = jacobi_large<R>(jobs[i], ws, E.stream, false, true, sweeps);
+      if (!conv) conv = jacobi_large<R>(jobs[i], lws, E.stream, false, true, sweeps);
       finish_large<R>(jobs[i], conv ? 1 : 0, sweeps, E.stream);
       E.counters[3]++;
     }

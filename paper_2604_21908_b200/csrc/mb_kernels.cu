@@ -1689,7 +1689,7 @@ int64_t large_pair_capacity(int64_t p) {
 template <typename R>
 static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const LargeScratch& ws,
                           cudaStream_t s, int& conv, int& sweeps, bool partials_ready,
-                          R* colnorm) {
+                          R* colnorm, int max_passes = 60) {
   static const int W2 = env_int("MB_JACOBI_W2", 32) == 64 ? 64 : (env_int("MB_JACOBI_W2", 32) == 16 ? 16 : 32);
   static const int inner = env_int("MB_JACOBI_INNER", 1);
   static const int debug = (MB_DEBUG_LOGS && env_int("MB_JACOBI_DEBUG", 0));
@@ -1747,7 +1747,7 @@ static void jacobi_sweeps(cx<R>* Xw, cx<R>* Vw, int64_t p, int64_t len, const La
       conv = 1;
       break;
     }
-    if (sweeps == 60) break;
+    if (sweeps == max_passes) break;
     ++sweeps;
     if (!dynamic || 2 * nopen > npair) {  // most pairs open: a full tournament sweep
       for (int rnd = 0; rnd < NB - 1; ++rnd) round(rnd, nullptr, nullptr, 0);
@@ -1846,7 +1846,7 @@ void finish_large(SvdJob<R>& J, int conv, int sweeps, cudaStream_t s) {
 // Returns whether every pair converged; `sweeps` accumulates the passes.
 template <typename R>
 bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fresh, bool perturb,
-                  int& sweeps) {
+                  int& sweeps, int max_passes) {
   const int64_t p = J.m < J.n ? J.m : J.n, q = J.m < J.n ? J.n : J.m;
   bool partials = false;
   if (fresh && J.A) {
@@ -1860,7 +1860,7 @@ bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fre
   }
   int conv = 0, sw = 0;
   // the final check launch leaves the column norms in sig[p, 2p)
-  jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sw, partials, J.sig + p);
+  jacobi_sweeps<R>(J.X, J.V, p, q, ws, s, conv, sw, partials, J.sig + p, max_passes);
   sweeps += sw;
   if (consume_forced_failure()) conv = 0;
   return conv != 0;
@@ -2251,7 +2251,7 @@ void launch_sample_pick(const cx<R>* amp, int64_t shots, int64_t r, const double
   template void launch_svd_small<R>(const SvdJob<R>*, int, int, cudaStream_t);                  \
   template void svd_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                     \
   template void finish_large<R>(SvdJob<R>&, int, int, cudaStream_t);                            \
-  template bool jacobi_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t, bool, bool, int&); \
+  template bool jacobi_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t, bool, bool, int&, int); \
   template void init_large<R>(SvdJob<R>&, const LargeScratch&, cudaStream_t);                  \
   template size_t large_workspace_elems<R>(int64_t, int64_t);                                   \
   template void launch_to_x<R>(const cx<R>*, cx<R>*, int64_t, int64_t, bool, cudaStream_t);     \

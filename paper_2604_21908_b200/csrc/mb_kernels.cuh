@@ -154,7 +154,7 @@ void svd_large(SvdJob<R>& job, const LargeScratch& ws, cudaStream_t s);
 // perturb = the reference's perturbed retry. Returns convergence.
 template <typename R>
 bool jacobi_large(SvdJob<R>& J, const LargeScratch& ws, cudaStream_t s, bool fresh, bool perturb,
-                  int& sweeps);
+                  int& sweeps, int max_passes = 60);
 
 // X (and V = I) from J.A, no sweeps
 template <typename R>
