@@ -286,7 +286,7 @@ static const int64_t kSeedJacobiP = getenv("MB_SEED_JACOBI_P") ? atoll(getenv("M
 // large jobs up to this width first get kTryPasses plain Jacobi passes
 // (MB_TRY_JACOBI_P, 0 = never)
 static const int64_t kTryJacobiP = getenv("MB_TRY_JACOBI_P") ? atoll(getenv("MB_TRY_JACOBI_P")) : 1024;
-static const int kTryPasses = getenv("MB_TRY_PASSES") ? atoi(getenv("MB_TRY_PASSES")) : 2;
+static const int kTryPasses = getenv("MB_TRY_PASSES") ? atoi(getenv("MB_TRY_PASSES")) : 3;
 
 template <typename R>
 static SvdJob<R> make_job(int slot, const cx<R>* A, int64_t m, int64_t n, double eps, int64_t chi,
