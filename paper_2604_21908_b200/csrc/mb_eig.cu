@@ -669,7 +669,7 @@ __global__ void k_copy_cols(const zd* __restrict__ src, zd* __restrict__ dst, in
 // completes a row tile (last of its nt contributions, counted with an atomic
 // per tile) reduces that tile's slots in a fixed order (k_symv_tiles2).
 constexpr int kST = 64;
-constexpr int kTileSmem = kST * (kST + 1) * 16;  // one complex128 tile, padded rows
+constexpr int kTileSmem = 32 * (kST + 1) * 16;  // half a complex128 tile, padded rows
 
 
 // ---- fused panel step (grid path): two launches per column --------------------
@@ -722,15 +722,22 @@ __global__ void __launch_bounds__(kRowBlk) k_trd_upd2(zd* __restrict__ A, int64_
   zd tp = mk<double>(0, 0);
   if (i > 0) {
     tp = tau[c - 1];
-    // p1 = V^H v, p2 = W^H v of the previous column (t < i - 1), per row tile
-    for (int e = threadIdx.x; e < 2 * tp_i; e += blockDim.x) {
-      const int t = e < tp_i ? e : kNB + (e - tp_i);
-      double re = 0, im = 0;
-      for (int bb = 0; bb < nt_prev; ++bb) {
-        re += part_p[(int64_t)bb * kPartStride + 2 * t];
-        im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
+    // p1 = V^H v, p2 = W^H v of the previous column (t < i - 1) from the
+    // per-row-tile partials: one warp per value, lanes strided over the row
+    // tiles, fixed-order butterfly (bitwise reproducible)
+    {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int e = wid; e < 2 * tp_i; e += nw) {
+        const int t = e < tp_i ? e : kNB + (e - tp_i);
+        double re = 0, im = 0;
+        for (int bb = lane; bb < nt_prev; bb += 32) {
+          re += part_p[(int64_t)bb * kPartStride + 2 * t];
+          im += part_p[(int64_t)bb * kPartStride + 2 * t + 1];
+        }
+        re = warp_sum(re);
+        im = warp_sum(im);
+        if (lane == 0) pv[t] = mk<double>(re, im);
       }
-      pv[t] = mk<double>(re, im);
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -785,16 +792,17 @@ __device__ __forceinline__ zd vload(const zd* __restrict__ A, int64_t n, int64_t
   return cmul(A[r + c * n], sc);
 }
 
-__global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, int64_t n, int64_t c,
+__global__ void __launch_bounds__(256, 3) k_symv_tiles2(const zd* __restrict__ A, int64_t n, int64_t c,
                                                      zd* __restrict__ VW, int i, int nt,
                                                      zd* __restrict__ P, int* __restrict__ cnt,
                                                      const double* __restrict__ part_x, int nblk_x,
                                                      double* __restrict__ ee, zd* __restrict__ tau,
                                                      zd* __restrict__ y, double* __restrict__ part_yv,
                                                      double* __restrict__ part_p) {
-  extern __shared__ zd tile[];  // kST x (kST + 1)
+  extern __shared__ zd tile[];  // 32 x (kST + 1): half a tile
   __shared__ zd vI[kST], vJ[kST];
-  __shared__ zd rowp[4][kST];
+  __shared__ zd rowp[1][kST];
+  __shared__ zd rowp8[8][kST];
   __shared__ zd colq[4][kST];
   __shared__ zd quarter[4][kST];
   __shared__ zd sh_sc;
@@ -846,31 +854,43 @@ __global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, i
     vJ[tid] = vload(A, n, c, c0 + tid, sc);
   }
   __syncthreads();
-  // the 64 x 64 tile staged in shared memory (16 independent loads per
-  // thread), then row sums (four threads per row) and column sums (four
-  // threads per column) straight from shared memory — no shuffle chains
-  const int64_t r = r0 + tr;
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int cc = tg * 16 + u;
-    const int64_t cg = c0 + cc;
-    tile[tr * (kST + 1) + cc] =
-        (r < n && cg < n && (I != J || tr >= cc)) ? A[r + cg * n] : mk<double>(0, 0);
-  }
-  __syncthreads();
+  // the 64 x 64 tile staged in shared memory in two 32-row halves (eight
+  // independent loads per thread each), row sums (eight threads per row)
+  // and column sums (four threads per column) straight from shared memory
   {
-    zd acc = mk<double>(0, 0);
-#pragma unroll
-    for (int u = 0; u < 16; ++u) acc = cadd(acc, cmul(tile[tr * (kST + 1) + tg * 16 + u], vJ[tg * 16 + u]));
-    rowp[tg][tr] = acc;
-    // column cc = tr over rows tg*16 .. tg*16+15 (strictly lower on the diagonal)
+    const int hr = tid & 31, g = tid >> 5;  // load / row-sum layout: row of the half, 8-column group
+    const int col = tid & 63, rg = tid >> 6;  // column-sum layout: column, 8-row group of the half
     zd cacc = mk<double>(0, 0);
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      const int rbase = half * 32;
+      const int64_t r = r0 + rbase + hr;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int rr = tg * 16 + u;
-      if (I != J || rr > tr) cacc = cadd(cacc, cmulc(tile[rr * (kST + 1) + tr], vI[rr]));
+      for (int u = 0; u < 8; ++u) {
+        const int cc = g * 8 + u;
+        const int64_t cg = c0 + cc;
+        tile[hr * (kST + 1) + cc] =
+            (r < n && cg < n && (I != J || rbase + hr >= cc)) ? A[r + cg * n] : mk<double>(0, 0);
+      }
+      __syncthreads();
+      zd acc = mk<double>(0, 0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = cadd(acc, cmul(tile[hr * (kST + 1) + g * 8 + u], vJ[g * 8 + u]));
+      rowp8[g][rbase + hr] = acc;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int hrow = rg * 8 + u, row = rbase + hrow;
+        if (I != J || row > col) cacc = cadd(cacc, cmulc(tile[hrow * (kST + 1) + col], vI[row]));
+      }
+      __syncthreads();
     }
-    colq[tg][tr] = cacc;
+    colq[rg][col] = cacc;
+    if (tid < kST) {
+      zd racc = mk<double>(0, 0);
+#pragma unroll
+      for (int gg = 0; gg < 8; ++gg) racc = cadd(racc, rowp8[gg][tid]);
+      rowp[0][tid] = racc;
+    }
   }
   const int lane = tid & 31;
   // diagonal tiles publish v and the partial V^H v, W^H v of their rows
@@ -911,8 +931,9 @@ __global__ void __launch_bounds__(256) k_symv_tiles2(const zd* __restrict__ A, i
     }
   zd* PI = P + ((int64_t)I * nt + J) * kST;
   zd* PJ = P + ((int64_t)J * nt + I) * kST;
+  __syncthreads();
   if (tid < kST) {
-    zd yv = cadd(cadd(rowp[0][tid], rowp[1][tid]), cadd(rowp[2][tid], rowp[3][tid]));
+    zd yv = rowp[0][tid];
     if (I == J) yv = cadd(yv, cadd(cadd(colq[0][tid], colq[1][tid]), cadd(colq[2][tid], colq[3][tid])));
     PI[tid] = yv;
   } else if (tid < 2 * kST && I != J) {
