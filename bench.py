@@ -275,8 +275,8 @@ def run_reference(args, rank, world):
 # the kernel behind each large-SVD stage (mb_eig.cu) and its bound
 _STAGE_KERNEL = {
     # stage: (kernel, bound, key in profiles/r02_kernel_traffic.json)
-    "trd_symv": ("k_symv_tiles2 + k_trd_upd2 (tridiagonalization, CUDA graph)", "hbm", "k_symv_tiles"),
-    "trd_panel": ("k_trd_upd2", "latency", "k_trd_upd"),
+    "trd_symv": ("k_symv_tiles2 + k_trd_upd2 (tridiagonalization, CUDA graph)", "hbm", "k_symv_tiles2"),
+    "trd_panel": ("k_trd_upd2", "latency", "k_trd_upd2"),
     "trd_update": ("k_gemm_cm<zd,zd,N,C>", "fp64", "k_gemm_cm"),
     "gram": ("k_gemm_cm<cx,zd,C,N>", "fp64", "k_gemm_cm"),
     "backtransform": ("k_gemm_cm<zd,zd,*,*>", "fp64", "k_gemm_cm"),
