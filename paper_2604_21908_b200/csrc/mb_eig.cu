@@ -685,16 +685,16 @@ constexpr int kTileSmem = 32 * (kST + 1) * 16;  // half a complex128 tile, padde
 // y_r - sum_{t < nt_} (W[r,t] p1[t] + V[r,t] p2[t]) with batched loads
 __device__ __forceinline__ zd row_corrected(zd yr, const zd* __restrict__ V, const zd* __restrict__ W,
                                            int64_t r, int64_t n, int nt_, const zd* pv) {
-  for (int t0 = 0; t0 < nt_; t0 += 16) {
-    zd vv[16], ww[16];
+  for (int t0 = 0; t0 < nt_; t0 += 8) {
+    zd vv[8], ww[8];
 #pragma unroll
-    for (int u = 0; u < 16; ++u)
+    for (int u = 0; u < 8; ++u)
       if (t0 + u < nt_) {
         vv[u] = V[r + (t0 + u) * n];
         ww[u] = W[r + (t0 + u) * n];
       }
 #pragma unroll
-    for (int u = 0; u < 16; ++u)
+    for (int u = 0; u < 8; ++u)
       if (t0 + u < nt_) {
         yr = csub(yr, cmul(ww[u], pv[t0 + u]));
         yr = csub(yr, cmul(vv[u], pv[kNB + t0 + u]));
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(kRowBlk) k_trd_upd2(zd* __restrict__ A, int64_
   __syncthreads();
   double xn = 0;
   if (r < n) {
-    const zd a = panel_row_update<16>(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, tp_i, wr);
+    const zd a = panel_row_update<8>(A[r + c * n], V, W, r, n, i, sh_rowv, sh_roww, tp_i, wr);
     A[r + c * n] = a;
     if (r == c) dd[c] = a.x;
     if (r >= c + 2) xn = cabs2(a);
