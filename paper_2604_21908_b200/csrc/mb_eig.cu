@@ -1317,7 +1317,6 @@ struct DcScratch {
   int* org;       // per root: origin pole
   double* tau;    // per root: offset from the origin
   double* zhat;
-  double rho_dummy;
 };
 
 // Deflation (one CTA per merge): z, sort, tolerance scan.
